@@ -1,0 +1,43 @@
+// Kernel-level entry points for the GPU tests (not part of the public
+// wavepipe.h contract): run one GEMM problem synchronously on the current
+// device so tests can compare each operand layout / epilogue against torch.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "capi_internal.hpp"
+#include "kernels/gemm.cuh"
+
+extern "C" int wp_debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype, const void* a, int64_t lda,
+                             int a_mn, int64_t a_b1, int64_t a_b2, const void* b, int64_t ldb, int b_mn,
+                             int64_t b_b1, int64_t b_b2, int mode, float alpha, void* c, int c_dtype, int64_t ldc,
+                             int64_t c_b1, int64_t c_b2, const float* bias, const void* resid, void* aux) {
+  try {
+    wpk::GemmProblem g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.nb1 = nb1;
+    g.nb2 = nb2;
+    g.in_dtype = in_dtype;
+    g.A = wpk::Operand{a, lda, a_mn != 0, a_b1, a_b2};
+    g.B = wpk::Operand{b, ldb, b_mn != 0, b_b1, b_b2};
+    g.epi.mode = mode;
+    g.epi.alpha = alpha;
+    g.epi.c = c;
+    g.epi.c_dtype = c_dtype;
+    g.epi.ldc = ldc;
+    g.epi.c_b1 = c_b1;
+    g.epi.c_b2 = c_b2;
+    g.epi.bias = bias;
+    g.epi.resid = resid;
+    g.epi.aux = aux;
+    wpk::gemm(g, nullptr);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return wpc::fail(WP_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
+    return WP_OK;
+  } catch (...) {
+    return wpc::map_exception();
+  }
+}

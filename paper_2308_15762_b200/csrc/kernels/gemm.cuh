@@ -1,0 +1,83 @@
+// GEMM interface shared by the tensor-core (bf16, tcgen05) and SIMT (fp32
+// parity mode) implementations.
+//
+//   C[z][m][n] (op)= sum_k A[z][m][k] * B[z][n][k]
+//
+// Each operand is row-major with a leading dimension; `mn_major` says which of
+// its two logical indices is contiguous:
+//   A: mn_major=false -> A[m][k] at ptr[m*ld + k]   (K-major, "row-major MxK")
+//      mn_major=true  -> A[m][k] at ptr[k*ld + m]   (M-major, "row-major KxM")
+//   B: mn_major=false -> B[n][k] at ptr[n*ld + k]   (K-major, torch Linear weight)
+//      mn_major=true  -> B[n][k] at ptr[k*ld + n]   (N-major)
+// so X @ W^T is (K,K), dY @ W is (K,N-major) and dY^T @ X is (M-major,N-major).
+// A two-level batch index z = z1 + nb1*z2 adds z1*b1 + z2*b2 elements to every
+// pointer (attention: z1 = head, z2 = sequence).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace wpk {
+
+enum DType : int { kF32 = 0, kBF16 = 1 };
+
+enum EpiMode : int {
+  kEpiStore = 0,     // C = alpha*acc (+ bias[n])
+  kEpiAccum = 1,     // C(f32) += alpha*acc              (gradient accumulation)
+  kEpiResidual = 2,  // C = resid + alpha*acc + bias[n]   (block output)
+  kEpiGelu = 3,      // aux = acc + bias (pre-activation), C = gelu(aux)
+  kEpiDGelu = 4,     // C = acc * gelu'(aux)              (aux = pre-activation)
+};
+
+struct Operand {
+  const void* ptr = nullptr;
+  int64_t ld = 0;
+  bool mn_major = false;
+  int64_t b1 = 0, b2 = 0;  // batch strides (elements)
+};
+
+struct Epilogue {
+  int mode = kEpiStore;
+  float alpha = 1.0f;
+  void* c = nullptr;  // dtype: c_dtype
+  int c_dtype = kBF16;
+  int64_t ldc = 0, c_b1 = 0, c_b2 = 0;
+  const float* bias = nullptr;  // [N] fp32, optional
+  const void* resid = nullptr;  // same dtype/ld as C (kEpiResidual)
+  void* aux = nullptr;          // same dtype/ld as C (kEpiGelu out, kEpiDGelu in)
+};
+
+struct GemmProblem {
+  int M = 0, N = 0, K = 0;
+  int nb1 = 1, nb2 = 1;
+  int in_dtype = kBF16;  // A and B element type
+  Operand A, B;
+  Epilogue epi;
+};
+
+// Launches on `stream`; returns the number of kernel launches issued (1).
+// Throws std::runtime_error on an unsupported problem.  gemm() dispatches on
+// in_dtype: bf16 -> gemm_tc (tcgen05), fp32 -> gemm_simt (FFMA parity mode).
+int gemm(const GemmProblem& p, cudaStream_t stream);
+int gemm_tc(const GemmProblem& p, cudaStream_t stream);
+int gemm_simt(const GemmProblem& p, cudaStream_t stream);
+
+#ifdef __CUDACC__
+// GELU, tanh approximation (GPT-2), and its derivative; shared by epilogues
+// and elementwise kernels so every path computes the same function.
+__device__ __forceinline__ float gelu_f(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float u = k0 * (x + k1 * x * x * x);
+  return 0.5f * x * (1.0f + tanhf(u));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float x2 = x * x;
+  const float u = k0 * (x + k1 * x2 * x);
+  const float t = tanhf(u);
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * (1.0f + 3.0f * k1 * x2);
+}
+#endif  // __CUDACC__
+
+}  // namespace wpk

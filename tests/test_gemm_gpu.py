@@ -1,0 +1,129 @@
+"""GEMM kernels vs a torch fp32 reference of the same contraction (GPU).
+
+Covers every operand-majorness combination the pipeline uses (X@W^T, dY@W,
+dY^T@X, attention's Q@K^T / P@V / P^T@dO), two-level batching, M/N/K tails
+and each fused epilogue, for both the tcgen05 bf16 kernel and the fp32 SIMT
+parity kernel.
+"""
+import ctypes as C
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_2308_15762_b200 import _native  # noqa: E402
+
+lib = _native.lib
+lib.wp_debug_gemm.restype = C.c_int
+lib.wp_debug_gemm.argtypes = [C.c_int] * 6 + [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int64] * 2 + \
+    [C.c_int, C.c_float, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+     C.c_void_p]
+
+EPI_STORE, EPI_ACCUM, EPI_RESID, EPI_GELU, EPI_DGELU = range(5)
+
+
+def gelu(x):
+    return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def gelu_grad(x):
+    t = torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3))
+    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x * x)
+
+
+def make_operand(rows, k, mn_major, dtype, batch=1):
+    """Logical [batch, rows, k] operand stored row-major as [.., rows, k] (K-major)
+    or [.., k, rows] (MN-major)."""
+    if mn_major:
+        store = torch.randn(batch, k, rows, device="cuda").to(dtype)
+        logical = store.float().transpose(1, 2)
+        ld = rows
+    else:
+        store = torch.randn(batch, rows, k, device="cuda").to(dtype)
+        logical = store.float()
+        ld = k
+    return store, logical, ld
+
+
+def run(M, N, K, a_mn, b_mn, dtype, mode=EPI_STORE, batch=1, bias=False, c_dtype=None, alpha=1.0):
+    c_dtype = c_dtype or dtype
+    in_code = 1 if dtype == torch.bfloat16 else 0
+    c_code = 1 if c_dtype == torch.bfloat16 else 0
+    a, al, lda = make_operand(M, K, a_mn, dtype, batch)
+    b, bl, ldb = make_operand(N, K, b_mn, dtype, batch)
+    acc = torch.bmm(al, bl.transpose(1, 2)) * alpha
+    bias_t = torch.randn(N, device="cuda") if bias else None
+    if bias_t is not None:
+        acc = acc + bias_t
+    c = torch.randn(batch, M, N, device="cuda").to(c_dtype)
+    resid = torch.randn(batch, M, N, device="cuda").to(c_dtype) if mode == EPI_RESID else None
+    aux = torch.randn(batch, M, N, device="cuda").to(c_dtype) if mode in (EPI_GELU, EPI_DGELU) else None
+    c0 = c.float().clone()
+    aux0 = aux.float().clone() if aux is not None else None
+    st = lib.wp_debug_gemm(M, N, K, batch, 1, in_code,
+                           a.data_ptr(), lda, int(a_mn), a[0].numel(), 0,
+                           b.data_ptr(), ldb, int(b_mn), b[0].numel(), 0,
+                           mode, alpha, c.data_ptr(), c_code, N, M * N, 0,
+                           bias_t.data_ptr() if bias_t is not None else None,
+                           resid.data_ptr() if resid is not None else None,
+                           aux.data_ptr() if aux is not None else None)
+    assert st == 0, lib.wp_last_error().decode()
+    torch.cuda.synchronize()
+    if mode == EPI_STORE:
+        ref = acc
+    elif mode == EPI_ACCUM:
+        ref = c0 + acc
+    elif mode == EPI_RESID:
+        ref = resid.float() + acc
+    elif mode == EPI_GELU:
+        pre = acc.to(c_dtype).float()
+        torch.testing.assert_close(aux.float(), pre, rtol=2e-2 if c_code else 1e-4, atol=2e-2 if c_code else 1e-4)
+        ref = gelu(pre)
+    else:
+        ref = acc * gelu_grad(aux0)
+    return c.float(), ref
+
+
+LAYOUTS = [(False, False), (False, True), (True, False), (True, True)]
+
+
+@pytest.mark.parametrize("a_mn,b_mn", LAYOUTS)
+@pytest.mark.parametrize("shape", [(256, 512, 256), (128, 256, 64), (200, 304, 136), (384, 1000, 512)])
+def test_tc_layouts(a_mn, b_mn, shape):
+    M, N, K = shape
+    out, ref = run(M, N, K, a_mn, b_mn, torch.bfloat16, c_dtype=torch.float32)
+    # bf16 inputs, fp32 accumulate: the reference uses the same bf16-rounded inputs.
+    torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-3 * K ** 0.5)
+
+
+@pytest.mark.parametrize("mode", [EPI_STORE, EPI_ACCUM, EPI_RESID, EPI_GELU, EPI_DGELU])
+def test_tc_epilogues(mode):
+    c_dtype = torch.float32 if mode == EPI_ACCUM else torch.bfloat16
+    out, ref = run(256, 768, 512, False, False, torch.bfloat16, mode=mode, bias=mode != EPI_DGELU,
+                   c_dtype=c_dtype)
+    tol = 1e-3 if c_dtype == torch.float32 else 2e-2
+    torch.testing.assert_close(out, ref, rtol=tol, atol=tol * 8)
+
+
+def test_tc_batched_alpha():
+    out, ref = run(128, 128, 64, False, False, torch.bfloat16, batch=6, alpha=0.125, c_dtype=torch.float32)
+    torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-2)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", LAYOUTS)
+@pytest.mark.parametrize("mode", [EPI_STORE, EPI_ACCUM, EPI_RESID, EPI_GELU, EPI_DGELU])
+def test_simt_fp32(a_mn, b_mn, mode):
+    out, ref = run(96, 130, 70, a_mn, b_mn, torch.float32, mode=mode, bias=mode != EPI_ACCUM, batch=2)
+    torch.testing.assert_close(out, ref, rtol=1e-5, atol=1e-4)
+
+
+def test_tc_large_throughput_sanity():
+    """One big K-major GEMM: correctness at scale (the bench measures speed)."""
+    M, N, K = 4096, 6144, 2048
+    out, ref = run(M, N, K, False, False, torch.bfloat16, c_dtype=torch.float32)
+    torch.testing.assert_close(out, ref, rtol=1e-3, atol=5e-2)
