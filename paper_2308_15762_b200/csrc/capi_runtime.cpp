@@ -1,0 +1,131 @@
+// C ABI of the GPU runtime (include/wavepipe.h, "GPU runtime" section).
+#include <cuda_runtime.h>
+
+#include <memory>
+
+#include "capi_internal.hpp"
+#include "runtime/runtime.hpp"
+
+struct wp_runtime {
+  std::unique_ptr<wprt::Runtime> rt;
+  wp_trace trace_view;
+};
+
+using wpc::fail;
+using wpc::map_exception;
+
+extern "C" {
+
+int wp_runtime_create(const wp_model_desc* model, const wp_list* list, int transport, const int* device_ids,
+                      int rank, const void* nccl_id, wp_runtime** out) {
+  try {
+    if (!model || !list || !out) return fail(WP_ERR_CONFIG, "null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      return fail(WP_ERR_CUDA, "no CUDA device available: the runtime has no CPU fallback");
+    }
+    auto* r = new wp_runtime;
+    try {
+      r->rt = std::make_unique<wprt::Runtime>(*model, list->list, transport, device_ids, rank, nccl_id);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    *out = r;
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+void wp_runtime_free(wp_runtime* rt) { delete rt; }
+
+int wp_train_step(wp_runtime* rt, const int32_t* tokens, const int32_t* labels, int on_device, float* loss) {
+  try {
+    if (!rt || !tokens || !labels) return fail(WP_ERR_CONFIG, "null argument");
+    const float l = rt->rt->train_step(tokens, labels, on_device != 0);
+    if (loss) *loss = l;
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int wp_runtime_trace(wp_runtime* rt, const wp_trace** trace) {
+  if (!rt || !trace) return fail(WP_ERR_CONFIG, "null argument");
+  rt->trace_view.trace = rt->rt->trace();
+  wpc::refresh(&rt->trace_view);
+  *trace = &rt->trace_view;
+  return WP_OK;
+}
+
+int wp_runtime_set_tracing(wp_runtime* rt, int enabled) {
+  if (!rt) return fail(WP_ERR_CONFIG, "null argument");
+  rt->rt->set_tracing(enabled != 0);
+  return WP_OK;
+}
+
+int wp_runtime_set_update(wp_runtime* rt, int enabled) {
+  if (!rt) return fail(WP_ERR_CONFIG, "null argument");
+  rt->rt->set_update(enabled != 0);
+  return WP_OK;
+}
+
+int wp_param_count(const wp_runtime* rt, int* count) {
+  if (!rt || !count) return fail(WP_ERR_CONFIG, "null argument");
+  *count = rt->rt->param_count();
+  return WP_OK;
+}
+
+int wp_param_info(const wp_runtime* rt, int index, const char** name, int64_t* numel, int* owned) {
+  try {
+    if (!rt) return fail(WP_ERR_CONFIG, "null argument");
+    bool own = false;
+    const auto& d = rt->rt->param_desc(index, &own);
+    if (name) *name = d.name.c_str();
+    if (numel) *numel = d.numel;
+    if (owned) *owned = own ? 1 : 0;
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int wp_get_param(wp_runtime* rt, const char* name, float* host_out, int64_t numel) {
+  try {
+    if (!rt || !name || !host_out) return fail(WP_ERR_CONFIG, "null argument");
+    rt->rt->get_param(name, host_out, numel, false);
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int wp_set_param(wp_runtime* rt, const char* name, const float* host_in, int64_t numel) {
+  try {
+    if (!rt || !name || !host_in) return fail(WP_ERR_CONFIG, "null argument");
+    rt->rt->set_param(name, host_in, numel);
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int wp_get_grad(wp_runtime* rt, const char* name, float* host_out, int64_t numel) {
+  try {
+    if (!rt || !name || !host_out) return fail(WP_ERR_CONFIG, "null argument");
+    rt->rt->get_param(name, host_out, numel, true);
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int wp_runtime_launch_count(const wp_runtime* rt, int64_t* launches) {
+  if (!rt || !launches) return fail(WP_ERR_CONFIG, "null argument");
+  *launches = rt->rt->launches();
+  return WP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,538 @@
+// HBM-bound kernels of the transformer stage: embedding, LayerNorm, attention
+// softmax, fused cross-entropy, bias-gradient reduction, optimizer, init.
+// Vectorised 16-byte accesses where the row is contiguous, one warp per row
+// for row-wise reductions (warp shuffles, no shared memory), block-level
+// partial sums + one global atomic per column for parameter gradients.
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <stdexcept>
+#include <string>
+
+#include "kernels/gemm.cuh"
+#include "kernels/ops.cuh"
+
+namespace wpk {
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(bf16 x) { return __bfloat162float(x); }
+template <typename T>
+__device__ __forceinline__ T from_f(float x);
+template <>
+__device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+// 8 contiguous elements <-> 8 floats (16 B for bf16, 32 B for fp32).
+__device__ __forceinline__ void load8(const float* p, float* v) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const bf16* p, float* v) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const bf16* h = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(h[i]);
+}
+__device__ __forceinline__ void store8(float* p, const float* v) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void store8(bf16* p, const float* v) {
+  uint4 u;
+  bf16* h = reinterpret_cast<bf16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) h[i] = __float2bfloat16_rn(v[i]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+void check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ embedding
+template <typename T>
+__global__ void embed_fwd_k(const int32_t* tok, const T* wte, const T* wpe, T* x, int T_, int seq, int h) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (i >= static_cast<int64_t>(T_) * h) return;
+  const int t = static_cast<int>(i / h), c = static_cast<int>(i % h);
+  float a[8], b[8];
+  load8(wte + static_cast<int64_t>(tok[t]) * h + c, a);
+  load8(wpe + static_cast<int64_t>(t % seq) * h + c, b);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] += b[k];
+  store8(x + i, a);
+}
+
+template <typename T>
+__global__ void embed_bwd_k(const int32_t* tok, const T* dx, float* dwte, float* dwpe, int T_, int seq, int h) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (i >= static_cast<int64_t>(T_) * h) return;
+  const int t = static_cast<int>(i / h), c = static_cast<int>(i % h);
+  float g[8];
+  load8(dx + i, g);
+  float* pw = dwte + static_cast<int64_t>(tok[t]) * h + c;
+  float* pp = dwpe + static_cast<int64_t>(t % seq) * h + c;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    atomicAdd(pw + k, g[k]);
+    atomicAdd(pp + k, g[k]);
+  }
+}
+
+// ------------------------------------------------------------------ layernorm
+// Lane l owns columns {l*8 + 256*c + j}: C = h/256 chunks of 8.
+template <typename T, int C>
+__global__ void __launch_bounds__(256) ln_fwd_k(const T* x, const float* w, const float* b, T* y, float* mean,
+                                                float* rstd, int T_, int h) {
+  const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= T_) return;
+  const T* xr = x + static_cast<int64_t>(row) * h;
+  float v[C][8];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    load8(xr + c * 256 + lane * 8, v[c]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[c][k];
+  }
+  const float mu = warp_sum(s) / h;
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q += (v[c][k] - mu) * (v[c][k] - mu);
+  const float rs = rsqrtf(warp_sum(q) / h + 1e-5f);
+  T* yr = y + static_cast<int64_t>(row) * h;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const int col = c * 256 + lane * 8;
+    float wv[8], bv[8], o[8];
+    load8(w + col, wv);
+    load8(b + col, bv);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = (v[c][k] - mu) * rs * wv[k] + bv[k];
+    store8(yr + col, o);
+  }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+// dx: warp per row, two passes over the (L1-resident) row so no per-column
+// state is held in registers.
+template <typename T, int C>
+__global__ void __launch_bounds__(256) ln_bwd_dx_k(const T* dy, const T* x, const float* mean, const float* rstd,
+                                                   const float* w, const T* dres, T* dx, int T_, int h) {
+  const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= T_) return;
+  const int64_t off = static_cast<int64_t>(row) * h;
+  const float mu = mean[row], rs = rstd[row];
+  float sg = 0.f, sgx = 0.f;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const int col = c * 256 + lane * 8;
+    float d[8], xv[8], wv[8];
+    load8(dy + off + col, d);
+    load8(x + off + col, xv);
+    load8(w + col, wv);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float g = d[k] * wv[k];
+      sg += g;
+      sgx += g * (xv[k] - mu) * rs;
+    }
+  }
+  sg = warp_sum(sg) / h;
+  sgx = warp_sum(sgx) / h;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const int col = c * 256 + lane * 8;
+    float d[8], xv[8], wv[8], r[8], o[8];
+    load8(dy + off + col, d);
+    load8(x + off + col, xv);
+    load8(w + col, wv);
+    if (dres) load8(dres + off + col, r);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      o[k] = rs * (d[k] * wv[k] - sg - (xv[k] - mu) * rs * sgx) + (dres ? r[k] : 0.f);
+    store8(dx + off + col, o);
+  }
+}
+
+// dw, db: lane <-> column (coalesced), 8 warps stride over a row range, block
+// partials reduced in shared memory, one atomic per column per block.
+template <typename T>
+__global__ void __launch_bounds__(256) ln_bwd_dwdb_k(const T* dy, const T* x, const float* mean, const float* rstd,
+                                                     float* dw, float* db, int T_, int h, int rows_per) {
+  __shared__ float sw[8][33], sb[8][33];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int col = blockIdx.x * 32 + lane;
+  const int r0 = blockIdx.y * rows_per, r1 = min(T_, r0 + rows_per);
+  float aw = 0.f, ab = 0.f;
+  if (col < h) {
+    for (int r = r0 + warp; r < r1; r += 8) {
+      const int64_t o = static_cast<int64_t>(r) * h + col;
+      const float d = to_f(dy[o]);
+      aw += d * (to_f(x[o]) - mean[r]) * rstd[r];
+      ab += d;
+    }
+  }
+  sw[warp][lane] = aw;
+  sb[warp][lane] = ab;
+  __syncthreads();
+  if (warp == 0 && col < h) {
+    float tw = 0.f, tb = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      tw += sw[i][lane];
+      tb += sb[i][lane];
+    }
+    atomicAdd(&dw[col], tw);
+    atomicAdd(&db[col], tb);
+  }
+}
+
+// ------------------------------------------------------------------- softmax
+// Warp per row; lane l holds columns l + 32*k.
+template <typename T>
+__global__ void __launch_bounds__(256) softmax_fwd_k(const float* S, T* P, int rows, int n, int causal) {
+  const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const int q = row % n;
+  const float* sr = S + static_cast<int64_t>(row) * n;
+  T* pr = P + static_cast<int64_t>(row) * n;
+  float v[32];
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int j = lane + 32 * k;
+    v[k] = (j < n && !(causal && j > q)) ? sr[j] : -INFINITY;
+    m = fmaxf(m, v[k]);
+  }
+  m = warp_max(m);
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    v[k] = (v[k] == -INFINITY) ? 0.f : __expf(v[k] - m);
+    s += v[k];
+  }
+  const float inv = 1.f / warp_sum(s);
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int j = lane + 32 * k;
+    if (j < n) pr[j] = from_f<T>(v[k] * inv);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) softmax_bwd_k(const float* dP, T* P, int rows, int n, float scale) {
+  const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const float* dr = dP + static_cast<int64_t>(row) * n;
+  T* pr = P + static_cast<int64_t>(row) * n;
+  float p[32], d[32];
+  float dot = 0.f;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int j = lane + 32 * k;
+    p[k] = j < n ? to_f(pr[j]) : 0.f;
+    d[k] = j < n ? dr[j] : 0.f;
+    dot += p[k] * d[k];
+  }
+  dot = warp_sum(dot);
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int j = lane + 32 * k;
+    if (j < n) pr[j] = from_f<T>(scale * p[k] * (d[k] - dot));
+  }
+}
+
+// -------------------------------------------------------------- cross-entropy
+template <typename T>
+__global__ void __launch_bounds__(256) xent_k(T* logits, const int32_t* labels, float* loss, int V, float loss_scale,
+                                              float grad_scale) {
+  const int row = blockIdx.x;
+  T* lr = logits + static_cast<int64_t>(row) * V;
+  float m = -INFINITY, s = 0.f;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) {
+    const float x = to_f(lr[j]);
+    if (x > m) {
+      s = s * __expf(m - x) + 1.f;
+      m = x;
+    } else {
+      s += __expf(x - m);
+    }
+  }
+  __shared__ float sm[32], ss[32];
+  // warp combine of (m, s)
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mm = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+    m = mm;
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (lane == 0) {
+    sm[warp] = m;
+    ss[warp] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x / 32;
+    m = lane < nw ? sm[lane] : -INFINITY;
+    s = lane < nw ? ss[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const float mm = fmaxf(m, m2);
+      s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+      m = mm;
+    }
+    if (lane == 0) {
+      sm[0] = m + logf(s);  // lse
+    }
+  }
+  __syncthreads();
+  const float lse = sm[0];
+  const int label = labels[row];
+  if (threadIdx.x == 0) atomicAdd(loss, (lse - to_f(lr[label])) * loss_scale);
+  __syncthreads();  // the label logit is read before being overwritten
+  for (int j = threadIdx.x; j < V; j += blockDim.x) {
+    const float p = __expf(to_f(lr[j]) - lse);
+    lr[j] = from_f<T>((p - (j == label ? 1.f : 0.f)) * grad_scale);
+  }
+}
+
+// --------------------------------------------------------------- bias grads
+template <typename T>
+__global__ void colsum_k(const T* dy, float* db, int T_, int n, int ld, int rows_per) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n) return;
+  const int r0 = blockIdx.y * rows_per, r1 = min(T_, r0 + rows_per);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += to_f(dy[static_cast<int64_t>(r) * ld + col]);
+  atomicAdd(&db[col], s);
+}
+
+// ---------------------------------------------------------------- optimizer
+__global__ void optim_k(OptimArgs a, float* w, float* g, float* m, float* v, bf16* shadow, int64_t n, float bc1,
+                        float bc2) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float p = w[i];
+    const float gr = g[i];
+    if (a.kind == 0) {
+      p -= a.lr * (gr + a.weight_decay * p);
+    } else {
+      const float mi = a.beta1 * m[i] + (1.f - a.beta1) * gr;
+      const float vi = a.beta2 * v[i] + (1.f - a.beta2) * gr * gr;
+      m[i] = mi;
+      v[i] = vi;
+      p -= a.lr * ((mi / bc1) / (sqrtf(vi / bc2) + a.eps) + a.weight_decay * p);
+    }
+    w[i] = p;
+    g[i] = 0.f;
+    if (shadow) shadow[i] = __float2bfloat16_rn(p);
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_normal_k(float* p, int64_t n, float std, uint64_t seed) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = mix64(seed ^ mix64(static_cast<uint64_t>(i)));
+    const float u1 = (static_cast<float>(r >> 40) + 1.f) * (1.f / 16777217.f);
+    const float u2 = static_cast<float>((r >> 16) & 0xFFFFFF) * (1.f / 16777216.f);
+    p[i] = std * sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+  }
+}
+
+__global__ void fill_k(float* p, int64_t n, float v) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void cast_k(const float* s, bf16* d, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[i] = __float2bfloat16_rn(s[i]);
+}
+
+int grid_for(int64_t n, int block, int cap = 148 * 16) {
+  return static_cast<int>(std::min<int64_t>((n + block - 1) / block, cap));
+}
+
+template <typename T>
+int ln_fwd_dispatch(const T* x, const float* w, const float* b, T* y, float* mean, float* rstd, int T_, int h,
+                    cudaStream_t s) {
+  const dim3 grid((T_ + 7) / 8), block(256);
+  switch (h / 256) {
+    case 1: ln_fwd_k<T, 1><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
+    case 2: ln_fwd_k<T, 2><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
+    case 4: ln_fwd_k<T, 4><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
+    case 8: ln_fwd_k<T, 8><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
+    case 16: ln_fwd_k<T, 16><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
+    default: throw std::runtime_error("layernorm: hidden must be 256 * {1,2,4,8,16}");
+  }
+  check_launch("layernorm_fwd");
+  return 1;
+}
+
+template <typename T>
+int ln_bwd_dispatch(const T* dy, const T* x, const float* mean, const float* rstd, const float* w, const T* dres,
+                    T* dx, float* dw, float* db, int T_, int h, cudaStream_t s) {
+  const dim3 grid((T_ + 7) / 8), block(256);
+  switch (h / 256) {
+    case 1: ln_bwd_dx_k<T, 1><<<grid, block, 0, s>>>(dy, x, mean, rstd, w, dres, dx, T_, h); break;
+    case 2: ln_bwd_dx_k<T, 2><<<grid, block, 0, s>>>(dy, x, mean, rstd, w, dres, dx, T_, h); break;
+    case 4: ln_bwd_dx_k<T, 4><<<grid, block, 0, s>>>(dy, x, mean, rstd, w, dres, dx, T_, h); break;
+    case 8: ln_bwd_dx_k<T, 8><<<grid, block, 0, s>>>(dy, x, mean, rstd, w, dres, dx, T_, h); break;
+    case 16: ln_bwd_dx_k<T, 16><<<grid, block, 0, s>>>(dy, x, mean, rstd, w, dres, dx, T_, h); break;
+    default: throw std::runtime_error("layernorm: hidden must be 256 * {1,2,4,8,16}");
+  }
+  check_launch("layernorm_bwd_dx");
+  const int rows_per = 256;
+  const dim3 g2((h + 31) / 32, (T_ + rows_per - 1) / rows_per);
+  ln_bwd_dwdb_k<T><<<g2, 256, 0, s>>>(dy, x, mean, rstd, dw, db, T_, h, rows_per);
+  check_launch("layernorm_bwd_dwdb");
+  return 2;
+}
+
+}  // namespace
+
+#define WP_DISPATCH(dtype, F, ...) \
+  ((dtype) == kBF16 ? F<bf16>(__VA_ARGS__) : F<float>(__VA_ARGS__))
+
+int embed_fwd(int dtype, const int32_t* tok, const void* wte, const void* wpe, void* x, int T_, int seq, int h,
+              cudaStream_t s) {
+  if (h % 8) throw std::runtime_error("embed: hidden must be a multiple of 8");
+  const int64_t n = static_cast<int64_t>(T_) * h / 8;
+  const int grid = static_cast<int>((n + 255) / 256);
+  if (dtype == kBF16)
+    embed_fwd_k<bf16><<<grid, 256, 0, s>>>(tok, static_cast<const bf16*>(wte), static_cast<const bf16*>(wpe),
+                                           static_cast<bf16*>(x), T_, seq, h);
+  else
+    embed_fwd_k<float><<<grid, 256, 0, s>>>(tok, static_cast<const float*>(wte), static_cast<const float*>(wpe),
+                                            static_cast<float*>(x), T_, seq, h);
+  check_launch("embed_fwd");
+  return 1;
+}
+
+int embed_bwd(int dtype, const int32_t* tok, const void* dx, float* dwte, float* dwpe, int T_, int seq, int h,
+              cudaStream_t s) {
+  const int64_t n = static_cast<int64_t>(T_) * h / 8;
+  const int grid = static_cast<int>((n + 255) / 256);
+  if (dtype == kBF16)
+    embed_bwd_k<bf16><<<grid, 256, 0, s>>>(tok, static_cast<const bf16*>(dx), dwte, dwpe, T_, seq, h);
+  else
+    embed_bwd_k<float><<<grid, 256, 0, s>>>(tok, static_cast<const float*>(dx), dwte, dwpe, T_, seq, h);
+  check_launch("embed_bwd");
+  return 1;
+}
+
+int layernorm_fwd(int dtype, const void* x, const float* w, const float* b, void* y, float* mean, float* rstd, int T_,
+                  int h, cudaStream_t s) {
+  if (dtype == kBF16)
+    return ln_fwd_dispatch<bf16>(static_cast<const bf16*>(x), w, b, static_cast<bf16*>(y), mean, rstd, T_, h, s);
+  return ln_fwd_dispatch<float>(static_cast<const float*>(x), w, b, static_cast<float*>(y), mean, rstd, T_, h, s);
+}
+
+int layernorm_bwd(int dtype, const void* dy, const void* x, const float* mean, const float* rstd, const float* w,
+                  const void* dres, void* dx, float* dw, float* db, int T_, int h, cudaStream_t s) {
+  if (dtype == kBF16)
+    return ln_bwd_dispatch<bf16>(static_cast<const bf16*>(dy), static_cast<const bf16*>(x), mean, rstd, w,
+                                 static_cast<const bf16*>(dres), static_cast<bf16*>(dx), dw, db, T_, h, s);
+  return ln_bwd_dispatch<float>(static_cast<const float*>(dy), static_cast<const float*>(x), mean, rstd, w,
+                                static_cast<const float*>(dres), static_cast<float*>(dx), dw, db, T_, h, s);
+}
+
+int softmax_fwd(int dtype, const float* S, void* P, int rows, int n, int causal, cudaStream_t s) {
+  if (n > 1024) throw std::runtime_error("softmax: row length must be <= 1024");
+  const int grid = (rows + 7) / 8;
+  if (dtype == kBF16) softmax_fwd_k<bf16><<<grid, 256, 0, s>>>(S, static_cast<bf16*>(P), rows, n, causal);
+  else softmax_fwd_k<float><<<grid, 256, 0, s>>>(S, static_cast<float*>(P), rows, n, causal);
+  check_launch("softmax_fwd");
+  return 1;
+}
+
+int softmax_bwd(int dtype, const float* dP, void* P, int rows, int n, float scale, cudaStream_t s) {
+  if (n > 1024) throw std::runtime_error("softmax: row length must be <= 1024");
+  const int grid = (rows + 7) / 8;
+  if (dtype == kBF16) softmax_bwd_k<bf16><<<grid, 256, 0, s>>>(dP, static_cast<bf16*>(P), rows, n, scale);
+  else softmax_bwd_k<float><<<grid, 256, 0, s>>>(dP, static_cast<float*>(P), rows, n, scale);
+  check_launch("softmax_bwd");
+  return 1;
+}
+
+int xent_fwd_bwd(int dtype, void* logits, const int32_t* labels, float* loss, int T_, int V, float loss_scale,
+                 float grad_scale, cudaStream_t s) {
+  if (dtype == kBF16)
+    xent_k<bf16><<<T_, 256, 0, s>>>(static_cast<bf16*>(logits), labels, loss, V, loss_scale, grad_scale);
+  else
+    xent_k<float><<<T_, 256, 0, s>>>(static_cast<float*>(logits), labels, loss, V, loss_scale, grad_scale);
+  check_launch("xent");
+  return 1;
+}
+
+int colsum_accum(int dtype, const void* dy, float* db, int T_, int n, int ld, cudaStream_t s) {
+  const int rows_per = 128;
+  const dim3 grid((n + 127) / 128, (T_ + rows_per - 1) / rows_per);
+  if (dtype == kBF16) colsum_k<bf16><<<grid, 128, 0, s>>>(static_cast<const bf16*>(dy), db, T_, n, ld, rows_per);
+  else colsum_k<float><<<grid, 128, 0, s>>>(static_cast<const float*>(dy), db, T_, n, ld, rows_per);
+  check_launch("colsum");
+  return 1;
+}
+
+int optimizer_step(const OptimArgs& a, float* w, float* g, float* m, float* v, void* shadow, int64_t n,
+                   cudaStream_t s) {
+  const float bc1 = 1.f - std::pow(a.beta1, static_cast<float>(a.step));
+  const float bc2 = 1.f - std::pow(a.beta2, static_cast<float>(a.step));
+  optim_k<<<grid_for(n, 256), 256, 0, s>>>(a, w, g, m, v, static_cast<bf16*>(shadow), n, bc1, bc2);
+  check_launch("optimizer");
+  return 1;
+}
+
+int init_normal(float* p, int64_t n, float std, uint64_t seed, cudaStream_t s) {
+  init_normal_k<<<grid_for(n, 256), 256, 0, s>>>(p, n, std, seed);
+  check_launch("init_normal");
+  return 1;
+}
+
+int fill_f32(float* p, int64_t n, float v, cudaStream_t s) {
+  fill_k<<<grid_for(n, 256), 256, 0, s>>>(p, n, v);
+  check_launch("fill");
+  return 1;
+}
+
+int cast_f32_to_bf16(const float* src, void* dst, int64_t n, cudaStream_t s) {
+  cast_k<<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<bf16*>(dst), n);
+  check_launch("cast");
+  return 1;
+}
+
+}  // namespace wpk

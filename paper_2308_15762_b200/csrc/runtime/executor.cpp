@@ -1,0 +1,858 @@
+// Runtime: parameters, stash pools and the per-device action interpreter.
+// See runtime.hpp for the executor contract and its reference citations.
+#include <cuda_bf16.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <stdexcept>
+
+#include "capi_internal.hpp"
+#include "runtime/runtime.hpp"
+
+namespace wprt {
+
+using wavepipe::Action;
+using wavepipe::ActionKind;
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw wpc::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ckn(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw wpc::CudaError(std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+struct DevGuard {
+  int prev = 0;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() { cudaSetDevice(prev); }
+};
+
+constexpr int kAct = static_cast<int>(wavepipe::Payload::Activation);
+constexpr int kGrad = static_cast<int>(wavepipe::Payload::Gradient);
+
+MsgKey key_of(const Action& a) {
+  const bool act = a.payload == kAct;
+  const bool out = a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange;
+  return MsgKey{a.payload, a.microbatch,
+                act ? (out ? a.slice_index : a.slice_index - 1) : (out ? a.slice_index - 1 : a.slice_index)};
+}
+
+uint64_t name_hash(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+  return h;
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------- pool
+Pool::~Pool() {
+  DevGuard g(dev_);
+  for (auto& b : all_) {
+    if (b->p) cudaFree(b->p);
+    if (b->ev) cudaEventDestroy(b->ev);
+  }
+}
+
+BufPtr Pool::alloc(size_t bytes, cudaStream_t stream, int cls) {
+  bytes = (bytes + 255) & ~size_t(255);
+  auto& fl = free_[{cls, bytes}];
+  if (!fl.empty()) {
+    BufPtr b = fl.back();
+    fl.pop_back();
+    if (b->ev_pending) {
+      ck(cudaStreamWaitEvent(stream, b->ev, 0), "pool wait");
+      b->ev_pending = false;
+    }
+    return b;
+  }
+  DevGuard g(dev_);
+  auto b = std::make_shared<Buf>();
+  ck(cudaMalloc(&b->p, bytes), "cudaMalloc (stash pool)");
+  b->bytes = bytes;
+  b->pool_class = cls;
+  reserved_ += bytes;
+  all_.push_back(b);
+  return b;
+}
+
+void Pool::release(const BufPtr& b, cudaStream_t stream) {
+  if (!b) return;
+  // Message buffers and anything released off the compute stream carry an
+  // event: the next owner (possibly another stream or device) waits on it.
+  if (b->pool_class == 1 || stream != home_) {
+    if (!b->ev) {
+      DevGuard g(dev_);
+      ck(cudaEventCreateWithFlags(&b->ev, cudaEventDisableTiming), "event create");
+    }
+    ck(cudaEventRecord(b->ev, stream), "pool release record");
+    b->ev_pending = true;
+  }
+  free_[{b->pool_class, b->bytes}].push_back(b);
+}
+
+// ------------------------------------------------------------- device state
+struct DeviceState {
+  int pipe = 0;  // pipeline device (index into the ActionList)
+  int cuda = 0;  // CUDA ordinal
+  cudaStream_t compute = nullptr, copy = nullptr;
+  std::unique_ptr<Pool> pool;
+  std::vector<ParamSlot> params;
+  std::unordered_map<std::string, int> by_name;
+  int64_t nparam = 0;
+  float *master = nullptr, *grad = nullptr, *m = nullptr, *v = nullptr;
+  void* shadow = nullptr;  // bf16 copy of master (bf16 mode)
+  float* loss = nullptr;
+  int32_t *tokens = nullptr, *labels = nullptr;
+  float* scores = nullptr;  // fp32 [mbs, heads, seq, seq] scratch
+  std::vector<std::pair<int, int>> be_partner;  // per position: (device, position) of a BE's counterpart
+
+  // per-step program state
+  size_t pc = 0;
+  std::map<std::pair<int, int>, SliceStash> stash;
+  std::map<MsgKey, BufPtr> handoff, inbox, outbox;
+  std::map<MsgKey, cudaEvent_t> outbox_ready;
+  std::vector<cudaEvent_t> pending;
+  cudaEvent_t last_start = nullptr;
+  cudaEvent_t step_begin = nullptr;
+  std::vector<cudaEvent_t> events;
+  size_t ev_next = 0;
+  std::vector<uint8_t> published_at;  // BE positions whose outgoing message is published
+
+  struct Rec {
+    int idx;
+    ActionKind kind;
+    int mb, slice;
+    cudaEvent_t s, e;
+  };
+  struct CommRec {
+    int src, dst;
+    cudaEvent_t post, arrive;
+    DeviceState* post_dev;
+    DeviceState* arrive_dev;
+  };
+  std::vector<Rec> recs;
+  std::vector<CommRec> comm_recs;
+};
+
+// ------------------------------------------------------------------ runtime
+Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, int transport, const int* device_ids,
+                 int rank, const void* nccl_id)
+    : m_(ModelSpec::from_desc(desc)), list_(list), transport_(transport), rank_(rank) {
+  const auto rep = wavepipe::validate_all(list_);
+  if (!rep.ok()) {
+    throw wavepipe::ScheduleError("action list fails validation:\n" + wavepipe::render_diagnostics_text(rep));
+  }
+  units_ = build_units(m_);
+  bounds_ = partition_units(units_, list_.config.stages);
+  const int P = list_.config.devices;
+  if (m_.tie && owner_device(0, 0) != owner_device(0, list_.config.stages - 1)) {
+    throw wavepipe::ConfigError(
+        "tie_embeddings needs the first and last slice on one device (true for Hanayo placements)");
+  }
+  if (transport_ != WP_TRANSPORT_LOCAL && transport_ != WP_TRANSPORT_NCCL) {
+    throw wavepipe::ConfigError("unknown transport");
+  }
+  if (transport_ == WP_TRANSPORT_NCCL && (rank_ < 0 || rank_ >= P || !nccl_id)) {
+    throw wavepipe::ConfigError("NCCL transport needs 0 <= rank < P and an ncclUniqueId");
+  }
+  build_devices(device_ids);
+  if (transport_ == WP_TRANSPORT_NCCL) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    DevGuard g(devs_[0]->cuda);
+    ncclComm_t comm;
+    ckn(ncclCommInitRank(&comm, P, id, rank_), "ncclCommInitRank");
+    nccl_comm_ = comm;
+  }
+}
+
+Runtime::~Runtime() {
+  if (nccl_comm_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_comm_));
+  for (auto& d : devs_) {
+    DevGuard g(d->cuda);
+    cudaDeviceSynchronize();
+    for (auto e : d->events) cudaEventDestroy(e);
+    if (d->step_begin) cudaEventDestroy(d->step_begin);
+    for (void* p : {static_cast<void*>(d->master), static_cast<void*>(d->grad), static_cast<void*>(d->m),
+                    static_cast<void*>(d->v), d->shadow, static_cast<void*>(d->loss), static_cast<void*>(d->tokens),
+                    static_cast<void*>(d->labels), static_cast<void*>(d->scores)})
+      if (p) cudaFree(p);
+    d->pool.reset();
+    if (d->compute) cudaStreamDestroy(d->compute);
+    if (d->copy) cudaStreamDestroy(d->copy);
+  }
+}
+
+int Runtime::owner_device(int mb, int slice) const {
+  return wavepipe::slice_owner(list_.config, list_.placement, slice,
+                               wavepipe::microbatch_direction(list_.config, mb))
+      .device;
+}
+
+void Runtime::build_devices(const int* device_ids) {
+  const int P = list_.config.devices;
+  dev_of_pipeline_.assign(P, -1);
+  std::vector<int> local;
+  if (transport_ == WP_TRANSPORT_LOCAL) {
+    for (int p = 0; p < P; ++p) local.push_back(p);
+  } else {
+    local.push_back(rank_);
+  }
+  const int B = list_.config.microbatches, T = m_.tokens();
+  for (size_t i = 0; i < local.size(); ++i) {
+    auto d = std::make_unique<DeviceState>();
+    d->pipe = local[i];
+    d->cuda = device_ids ? device_ids[transport_ == WP_TRANSPORT_LOCAL ? i : 0] : 0;
+    dev_of_pipeline_[d->pipe] = static_cast<int>(i);
+    DevGuard g(d->cuda);
+    ck(cudaStreamCreateWithFlags(&d->compute, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&d->copy, cudaStreamNonBlocking), "stream");
+    d->pool = std::make_unique<Pool>(d->cuda, d->compute);
+    ck(cudaEventCreate(&d->step_begin), "event");
+    // Parameters of every unit of every slice this device holds.
+    std::vector<int> mine;
+    for (int s : [&] {
+           std::vector<int> v;
+           for (const auto& sl : list_.placement.assignment[d->pipe]) v.push_back(sl.index);
+           return v;
+         }()) {
+      for (int u = bounds_[s]; u < bounds_[s + 1]; ++u) mine.push_back(u);
+    }
+    std::sort(mine.begin(), mine.end());
+    int64_t off = 0;
+    for (int u : mine) {
+      for (auto& pd : unit_params(m_, u, units_[u])) {
+        ParamSlot slot;
+        slot.desc = pd;
+        slot.offset = off;
+        off += (pd.numel + 63) / 64 * 64;
+        d->by_name[pd.name] = static_cast<int>(d->params.size());
+        param_index_[pd.name] = ParamRef{static_cast<int>(i), static_cast<int>(d->params.size()), pd};
+        param_names_.push_back(pd.name);
+        d->params.push_back(slot);
+      }
+    }
+    d->nparam = std::max<int64_t>(off, 64);
+    const size_t pb = d->nparam * sizeof(float);
+    ck(cudaMalloc(&d->master, pb), "cudaMalloc params");
+    ck(cudaMalloc(&d->grad, pb), "cudaMalloc grads");
+    ck(cudaMemset(d->grad, 0, pb), "memset");
+    if (m_.optimizer == 1) {
+      ck(cudaMalloc(&d->m, pb), "cudaMalloc adam m");
+      ck(cudaMalloc(&d->v, pb), "cudaMalloc adam v");
+      ck(cudaMemset(d->m, 0, pb), "memset");
+      ck(cudaMemset(d->v, 0, pb), "memset");
+    }
+    if (m_.dtype == wpk::kBF16) ck(cudaMalloc(&d->shadow, d->nparam * 2), "cudaMalloc shadow");
+    ck(cudaMalloc(&d->loss, sizeof(float)), "cudaMalloc loss");
+    ck(cudaMalloc(&d->tokens, sizeof(int32_t) * B * T), "cudaMalloc tokens");
+    ck(cudaMalloc(&d->labels, sizeof(int32_t) * B * T), "cudaMalloc labels");
+    const size_t sc = sizeof(float) * size_t(m_.mbs) * m_.heads * m_.seq * m_.seq;
+    ck(cudaMalloc(&d->scores, sc), "cudaMalloc scores");
+    init_params(*d);
+    ck(cudaDeviceSynchronize(), "init sync");
+    devs_.push_back(std::move(d));
+  }
+  // BE counterparts, resolved once (ref include/wavepipe/action.hpp:67-73).
+  std::map<int, std::vector<std::pair<int, int>>> groups;
+  for (int p = 0; p < P; ++p)
+    for (int i = 0; i < static_cast<int>(list_.per_device[p].size()); ++i)
+      if (list_.per_device[p][i].kind == ActionKind::BatchedExchange)
+        groups[list_.per_device[p][i].batch_group].push_back({p, i});
+  for (auto& d : devs_) d->be_partner.assign(list_.per_device[d->pipe].size(), {-1, -1});
+  for (auto& [g, ends] : groups) {
+    for (int k = 0; k < 2; ++k) {
+      const int li = dev_of_pipeline_[ends[k].first];
+      if (li >= 0) devs_[li]->be_partner[ends[k].second] = ends[1 - k];
+    }
+  }
+}
+
+void Runtime::init_params(DeviceState& d) {
+  for (auto& s : d.params) {
+    float* p = d.master + s.offset;
+    if (s.desc.init_std > 0) {
+      launches_ += wpk::init_normal(p, s.desc.numel, s.desc.init_std, m_.seed ^ name_hash(s.desc.name), d.compute);
+    } else {
+      launches_ += wpk::fill_f32(p, s.desc.numel, s.desc.init_value, d.compute);
+    }
+  }
+  if (d.shadow) launches_ += wpk::cast_f32_to_bf16(d.master, d.shadow, d.nparam, d.compute);
+}
+
+const void* Runtime::weight(DeviceState& d, const std::string& name) const {
+  auto it = d.by_name.find(name);
+  if (it == d.by_name.end()) throw std::runtime_error("parameter not on this device: " + name);
+  const int64_t off = d.params[it->second].offset;
+  if (m_.dtype == wpk::kBF16) return static_cast<const __nv_bfloat16*>(d.shadow) + off;
+  return d.master + off;
+}
+
+float* Runtime::master(DeviceState& d, const std::string& name) const {
+  auto it = d.by_name.find(name);
+  if (it == d.by_name.end()) throw std::runtime_error("parameter not on this device: " + name);
+  return d.master + d.params[it->second].offset;
+}
+
+float* Runtime::grad(DeviceState& d, const std::string& name) const {
+  auto it = d.by_name.find(name);
+  if (it == d.by_name.end()) throw std::runtime_error("parameter not on this device: " + name);
+  return d.grad + d.params[it->second].offset;
+}
+
+void Runtime::gemm(DeviceState& d, const wpk::GemmProblem& g) { launches_ += wpk::gemm(g, d.compute); }
+
+cudaEvent_t Runtime::next_event(DeviceState& d) {
+  if (d.ev_next == d.events.size()) {
+    DevGuard g(d.cuda);
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "event create");
+    d.events.push_back(e);
+  }
+  return d.events[d.ev_next++];
+}
+
+// ------------------------------------------------------------ unit kernels
+namespace {
+
+wpk::Operand op(const void* p, int64_t ld, bool mn, int64_t b1 = 0, int64_t b2 = 0) {
+  return wpk::Operand{p, ld, mn, b1, b2};
+}
+
+void* at(const BufPtr& b, int64_t elems, int es) { return static_cast<char*>(b->p) + elems * es; }
+
+}  // namespace
+
+BufPtr Runtime::unit_fwd(DeviceState& d, int ui, int mb, BufPtr x, UnitStash& st) {
+  const Unit& u = units_[ui];
+  const int T = m_.tokens(), h = m_.hidden, f = m_.ffn, V = m_.vocab, S = m_.seq, H = m_.heads, dh = m_.head_dim();
+  const int es = m_.act_bytes(), dt = m_.dtype;
+  cudaStream_t cs = d.compute;
+  Pool& pool = *d.pool;
+  auto act = [&](int64_t n) { return pool.alloc(n * es, cs, 0); };
+  auto f32 = [&](int64_t n) { return pool.alloc(n * 4, cs, 0); };
+  const std::string L = "h." + std::to_string(u.layer) + ".";
+
+  if (u.kind == UnitKind::Embed) {
+    BufPtr out = act(int64_t(T) * h);
+    launches_ += wpk::embed_fwd(dt, d.tokens + int64_t(mb) * T, weight(d, "wte"), weight(d, "wpe"), out->p, T, S, h,
+                                cs);
+    return out;
+  }
+  st.x = x;
+  st.ln = act(int64_t(T) * h);
+  st.mean = f32(T);
+  st.rstd = f32(T);
+  const char* lnw = u.kind == UnitKind::Attn ? "ln1" : u.kind == UnitKind::Mlp ? "ln2" : nullptr;
+  const std::string lnname = u.kind == UnitKind::Head ? "lnf" : L + lnw;
+  launches_ += wpk::layernorm_fwd(dt, x->p, master(d, lnname + ".w"), master(d, lnname + ".b"), st.ln->p,
+                                  static_cast<float*>(st.mean->p), static_cast<float*>(st.rstd->p), T, h, cs);
+  wpk::GemmProblem g;
+  g.in_dtype = dt;
+  if (u.kind == UnitKind::Attn) {
+    st.a = act(int64_t(T) * 3 * h);  // qkv
+    g.M = T, g.N = 3 * h, g.K = h;
+    g.A = op(st.ln->p, h, false);
+    g.B = op(weight(d, L + "attn.qkv.w"), h, false);
+    g.epi.c = st.a->p, g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.bias = master(d, L + "attn.qkv.b");
+    gemm(d, g);
+    // S = Q K^T / sqrt(d), per (head, sequence)
+    wpk::GemmProblem sg;
+    sg.in_dtype = dt;
+    sg.M = S, sg.N = S, sg.K = dh, sg.nb1 = H, sg.nb2 = m_.mbs;
+    sg.A = op(st.a->p, 3 * h, false, dh, int64_t(S) * 3 * h);
+    sg.B = op(at(st.a, h, es), 3 * h, false, dh, int64_t(S) * 3 * h);
+    sg.epi.c = d.scores, sg.epi.c_dtype = wpk::kF32, sg.epi.ldc = S, sg.epi.c_b1 = int64_t(S) * S,
+    sg.epi.c_b2 = int64_t(H) * S * S, sg.epi.alpha = 1.0f / std::sqrt(static_cast<float>(dh));
+    gemm(d, sg);
+    st.b = act(int64_t(m_.mbs) * H * S * S);  // P
+    launches_ += wpk::softmax_fwd(dt, d.scores, st.b->p, m_.mbs * H * S, S, m_.causal, cs);
+    // ctx = P V
+    st.c = act(int64_t(T) * h);
+    wpk::GemmProblem pv;
+    pv.in_dtype = dt;
+    pv.M = S, pv.N = dh, pv.K = S, pv.nb1 = H, pv.nb2 = m_.mbs;
+    pv.A = op(st.b->p, S, false, int64_t(S) * S, int64_t(H) * S * S);
+    pv.B = op(at(st.a, 2 * h, es), 3 * h, true, dh, int64_t(S) * 3 * h);
+    pv.epi.c = st.c->p, pv.epi.c_dtype = dt, pv.epi.ldc = h, pv.epi.c_b1 = dh, pv.epi.c_b2 = int64_t(S) * h;
+    gemm(d, pv);
+    BufPtr out = act(int64_t(T) * h);
+    wpk::GemmProblem pr;
+    pr.in_dtype = dt;
+    pr.M = T, pr.N = h, pr.K = h;
+    pr.A = op(st.c->p, h, false);
+    pr.B = op(weight(d, L + "attn.proj.w"), h, false);
+    pr.epi.mode = wpk::kEpiResidual, pr.epi.c = out->p, pr.epi.c_dtype = dt, pr.epi.ldc = h,
+    pr.epi.bias = master(d, L + "attn.proj.b"), pr.epi.resid = x->p;
+    gemm(d, pr);
+    return out;
+  }
+  if (u.kind == UnitKind::Mlp) {
+    st.a = act(int64_t(T) * f);  // pre-activation u
+    st.b = act(int64_t(T) * f);  // gelu(u)
+    g.M = T, g.N = f, g.K = h;
+    g.A = op(st.ln->p, h, false);
+    g.B = op(weight(d, L + "mlp.fc1.w"), h, false);
+    g.epi.mode = wpk::kEpiGelu, g.epi.c = st.b->p, g.epi.aux = st.a->p, g.epi.c_dtype = dt, g.epi.ldc = f,
+    g.epi.bias = master(d, L + "mlp.fc1.b");
+    gemm(d, g);
+    BufPtr out = act(int64_t(T) * h);
+    wpk::GemmProblem g2;
+    g2.in_dtype = dt;
+    g2.M = T, g2.N = h, g2.K = f;
+    g2.A = op(st.b->p, f, false);
+    g2.B = op(weight(d, L + "mlp.fc2.w"), f, false);
+    g2.epi.mode = wpk::kEpiResidual, g2.epi.c = out->p, g2.epi.c_dtype = dt, g2.epi.ldc = h,
+    g2.epi.bias = master(d, L + "mlp.fc2.b"), g2.epi.resid = x->p;
+    gemm(d, g2);
+    return out;
+  }
+  // Head: logits, fused cross-entropy (loss + dlogits in place).
+  st.a = act(int64_t(T) * V);
+  g.M = T, g.N = V, g.K = h;
+  g.A = op(st.ln->p, h, false);
+  g.B = op(weight(d, m_.tie ? "wte" : "lm_head.w"), h, false);
+  g.epi.c = st.a->p, g.epi.c_dtype = dt, g.epi.ldc = V;
+  gemm(d, g);
+  const float scale = 1.0f / (static_cast<float>(T) * list_.config.microbatches);
+  launches_ += wpk::xent_fwd_bwd(dt, st.a->p, d.labels + int64_t(mb) * T, d.loss, T, V, scale, scale, cs);
+  return nullptr;
+}
+
+BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr dy) {
+  const Unit& u = units_[ui];
+  const int T = m_.tokens(), h = m_.hidden, f = m_.ffn, V = m_.vocab, S = m_.seq, H = m_.heads, dh = m_.head_dim();
+  const int es = m_.act_bytes(), dt = m_.dtype;
+  cudaStream_t cs = d.compute;
+  Pool& pool = *d.pool;
+  auto act = [&](int64_t n) { return pool.alloc(n * es, cs, 0); };
+  auto drop = [&](BufPtr& b) {
+    pool.release(b, cs);
+    b.reset();
+  };
+  const std::string L = "h." + std::to_string(u.layer) + ".";
+
+  if (u.kind == UnitKind::Embed) {
+    launches_ += wpk::embed_bwd(dt, d.tokens + int64_t(mb) * T, dy->p, grad(d, "wte"), grad(d, "wpe"), T, S, h, cs);
+    drop(dy);
+    return nullptr;
+  }
+  // dX = dY W  (B N-major: W[k][n] with k = out features)
+  auto dgrad = [&](const void* dY, int ld_dy, int n_out, const void* W, int n_in, void* dX, int mode = wpk::kEpiStore,
+                   const void* aux = nullptr) {
+    wpk::GemmProblem g;
+    g.in_dtype = dt;
+    g.M = T, g.N = n_in, g.K = n_out;
+    g.A = op(dY, ld_dy, false);
+    g.B = op(W, n_in, true);
+    g.epi.mode = mode, g.epi.c = dX, g.epi.c_dtype = dt, g.epi.ldc = n_in, g.epi.aux = const_cast<void*>(aux);
+    gemm(d, g);
+  };
+  // dW += dY^T X  (both operands MN-major over the token dimension)
+  auto wgrad = [&](const void* dY, int n_out, const void* X, int n_in, float* dW) {
+    wpk::GemmProblem g;
+    g.in_dtype = dt;
+    g.M = n_out, g.N = n_in, g.K = T;
+    g.A = op(dY, n_out, true);
+    g.B = op(X, n_in, true);
+    g.epi.mode = wpk::kEpiAccum, g.epi.c = dW, g.epi.c_dtype = wpk::kF32, g.epi.ldc = n_in;
+    gemm(d, g);
+  };
+  auto ln_bwd = [&](const BufPtr& dln, const std::string& name, const BufPtr& dres) {
+    BufPtr dx = act(int64_t(T) * h);
+    launches_ += wpk::layernorm_bwd(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p),
+                                    static_cast<float*>(st.rstd->p), master(d, name + ".w"),
+                                    dres ? dres->p : nullptr, dx->p, grad(d, name + ".w"), grad(d, name + ".b"), T, h,
+                                    cs);
+    return dx;
+  };
+
+  if (u.kind == UnitKind::Head) {
+    const std::string wn = m_.tie ? "wte" : "lm_head.w";
+    BufPtr dln = act(int64_t(T) * h);
+    dgrad(st.a->p, V, V, weight(d, wn), h, dln->p);
+    wgrad(st.a->p, V, st.ln->p, h, grad(d, wn));
+    BufPtr dx = ln_bwd(dln, "lnf", nullptr);
+    drop(dln);
+    for (BufPtr* b : {&st.x, &st.ln, &st.mean, &st.rstd, &st.a}) drop(*b);
+    if (dy) drop(dy);
+    return dx;
+  }
+  if (u.kind == UnitKind::Mlp) {
+    BufPtr du = act(int64_t(T) * f);
+    dgrad(dy->p, h, h, weight(d, L + "mlp.fc2.w"), f, du->p, wpk::kEpiDGelu, st.a->p);
+    wgrad(dy->p, h, st.b->p, f, grad(d, L + "mlp.fc2.w"));
+    launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "mlp.fc2.b"), T, h, h, cs);
+    wgrad(du->p, f, st.ln->p, h, grad(d, L + "mlp.fc1.w"));
+    launches_ += wpk::colsum_accum(dt, du->p, grad(d, L + "mlp.fc1.b"), T, f, f, cs);
+    BufPtr dln = act(int64_t(T) * h);
+    dgrad(du->p, f, f, weight(d, L + "mlp.fc1.w"), h, dln->p);
+    BufPtr dx = ln_bwd(dln, L + "ln2", dy);
+    drop(du);
+    drop(dln);
+    drop(dy);
+    for (BufPtr* b : {&st.x, &st.ln, &st.mean, &st.rstd, &st.a, &st.b}) drop(*b);
+    return dx;
+  }
+  // Attention block.
+  BufPtr dctx = act(int64_t(T) * h);
+  dgrad(dy->p, h, h, weight(d, L + "attn.proj.w"), h, dctx->p);
+  wgrad(dy->p, h, st.c->p, h, grad(d, L + "attn.proj.w"));
+  launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "attn.proj.b"), T, h, h, cs);
+  // dP = dctx V^T  (fp32 scratch)
+  {
+    wpk::GemmProblem g;
+    g.in_dtype = dt;
+    g.M = S, g.N = S, g.K = dh, g.nb1 = H, g.nb2 = m_.mbs;
+    g.A = op(dctx->p, h, false, dh, int64_t(S) * h);
+    g.B = op(at(st.a, 2 * h, es), 3 * h, false, dh, int64_t(S) * 3 * h);
+    g.epi.c = d.scores, g.epi.c_dtype = wpk::kF32, g.epi.ldc = S, g.epi.c_b1 = int64_t(S) * S,
+    g.epi.c_b2 = int64_t(H) * S * S;
+    gemm(d, g);
+  }
+  BufPtr dqkv = act(int64_t(T) * 3 * h);
+  // dV = P^T dctx
+  {
+    wpk::GemmProblem g;
+    g.in_dtype = dt;
+    g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
+    g.A = op(st.b->p, S, true, int64_t(S) * S, int64_t(H) * S * S);
+    g.B = op(dctx->p, h, true, dh, int64_t(S) * h);
+    g.epi.c = at(dqkv, 2 * h, es), g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh,
+    g.epi.c_b2 = int64_t(S) * 3 * h;
+    gemm(d, g);
+  }
+  // dS = P * (dP - rowsum(dP * P)) / sqrt(d), in place over P
+  launches_ += wpk::softmax_bwd(dt, d.scores, st.b->p, m_.mbs * H * S, S, 1.0f / std::sqrt(static_cast<float>(dh)),
+                                cs);
+  // dQ = dS K
+  {
+    wpk::GemmProblem g;
+    g.in_dtype = dt;
+    g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
+    g.A = op(st.b->p, S, false, int64_t(S) * S, int64_t(H) * S * S);
+    g.B = op(at(st.a, h, es), 3 * h, true, dh, int64_t(S) * 3 * h);
+    g.epi.c = dqkv->p, g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh, g.epi.c_b2 = int64_t(S) * 3 * h;
+    gemm(d, g);
+  }
+  // dK = dS^T Q
+  {
+    wpk::GemmProblem g;
+    g.in_dtype = dt;
+    g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
+    g.A = op(st.b->p, S, true, int64_t(S) * S, int64_t(H) * S * S);
+    g.B = op(st.a->p, 3 * h, true, dh, int64_t(S) * 3 * h);
+    g.epi.c = at(dqkv, h, es), g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh,
+    g.epi.c_b2 = int64_t(S) * 3 * h;
+    gemm(d, g);
+  }
+  wgrad(dqkv->p, 3 * h, st.ln->p, h, grad(d, L + "attn.qkv.w"));
+  launches_ += wpk::colsum_accum(dt, dqkv->p, grad(d, L + "attn.qkv.b"), T, 3 * h, 3 * h, cs);
+  BufPtr dln = act(int64_t(T) * h);
+  dgrad(dqkv->p, 3 * h, 3 * h, weight(d, L + "attn.qkv.w"), h, dln->p);
+  BufPtr dx = ln_bwd(dln, L + "ln1", dy);
+  drop(dctx);
+  drop(dqkv);
+  drop(dln);
+  drop(dy);
+  for (BufPtr* b : {&st.x, &st.ln, &st.mean, &st.rstd, &st.a, &st.b, &st.c}) drop(*b);
+  return dx;
+}
+
+// ---------------------------------------------------------- message plumbing
+BufPtr Runtime::take_input(DeviceState& d, const MsgKey& k) {
+  for (auto* box : {&d.handoff, &d.inbox}) {
+    auto it = box->find(k);
+    if (it != box->end()) {
+      BufPtr b = it->second;
+      box->erase(it);
+      return b;
+    }
+  }
+  throw wavepipe::SimulationError("runtime: input message (payload " + std::to_string(k.payload) + ", microbatch " +
+                                  std::to_string(k.mb) + ", boundary " + std::to_string(k.low) + ") never arrived");
+}
+
+void Runtime::deliver(DeviceState& d, const MsgKey& k, BufPtr buf) {
+  const int consumer = k.payload == kAct ? k.low + 1 : k.low;
+  if (owner_device(k.mb, consumer) == d.pipe) {
+    d.handoff[k] = buf;
+    return;
+  }
+  d.outbox[k] = buf;
+  cudaEvent_t e = next_event(d);
+  ck(cudaEventRecord(e, d.compute), "record ready");
+  d.outbox_ready[k] = e;
+}
+
+void Runtime::post_copy(DeviceState& dst, const MsgKey& k, Published msg) {
+  DeviceState& src = *devs_[dev_of_pipeline_[msg.src]];
+  const size_t bytes = msg.buf->bytes;
+  BufPtr landing = dst.pool->alloc(bytes, src.copy, 1);
+  cudaEvent_t post = dst.last_start ? dst.last_start : dst.step_begin;
+  ck(cudaStreamWaitEvent(src.copy, post, 0), "wait post");
+  ck(cudaStreamWaitEvent(src.copy, msg.ready, 0), "wait ready");
+  if (src.cuda == dst.cuda) {
+    ck(cudaMemcpyAsync(landing->p, msg.buf->p, bytes, cudaMemcpyDeviceToDevice, src.copy), "D2D copy");
+  } else {
+    ck(cudaMemcpyPeerAsync(landing->p, dst.cuda, msg.buf->p, src.cuda, bytes, src.copy), "peer copy");
+  }
+  cudaEvent_t arrive = next_event(src);
+  ck(cudaEventRecord(arrive, src.copy), "record arrival");
+  src.pool->release(msg.buf, src.copy);
+  dst.pending.push_back(arrive);
+  dst.inbox[k] = landing;
+  if (tracing_) dst.comm_recs.push_back({msg.src, dst.pipe, post, arrive, &dst, &src});
+}
+
+// --------------------------------------------------------------- execution
+void Runtime::forward(DeviceState& d, const Action& a) {
+  const int b = a.microbatch, s = a.slice_index;
+  BufPtr x = s == 0 ? nullptr : take_input(d, MsgKey{kAct, b, s - 1});
+  SliceStash& st = d.stash[{b, s}];
+  st.units.assign(bounds_[s + 1] - bounds_[s], UnitStash{});
+  for (int u = bounds_[s]; u < bounds_[s + 1]; ++u) x = unit_fwd(d, u, b, x, st.units[u - bounds_[s]]);
+  if (s < list_.config.stages - 1) deliver(d, MsgKey{kAct, b, s}, x);
+}
+
+void Runtime::backward(DeviceState& d, const Action& a) {
+  const int b = a.microbatch, s = a.slice_index;
+  BufPtr dy = s == list_.config.stages - 1 ? nullptr : take_input(d, MsgKey{kGrad, b, s});
+  auto it = d.stash.find({b, s});
+  if (it == d.stash.end()) throw wavepipe::SimulationError("runtime: backward before forward");
+  SliceStash st = std::move(it->second);
+  d.stash.erase(it);
+  for (int u = bounds_[s + 1] - 1; u >= bounds_[s]; --u) dy = unit_bwd(d, u, b, st.units[u - bounds_[s]], dy);
+  if (s > 0) deliver(d, MsgKey{kGrad, b, s - 1}, dy);
+}
+
+void Runtime::optimizer(DeviceState& d) {
+  if (!update_) return;
+  wpk::OptimArgs o{m_.optimizer, m_.lr, m_.beta1, m_.beta2, m_.eps, m_.weight_decay, step_ + 1};
+  launches_ += wpk::optimizer_step(o, d.master, d.grad, d.m, d.v, d.shadow, d.nparam, d.compute);
+}
+
+bool Runtime::advance(DeviceState& d) {
+  const auto& prog = list_.per_device[d.pipe];
+  bool moved = false;
+  DevGuard g(d.cuda);
+  ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm_);
+  while (d.pc < prog.size()) {
+    const Action& a = prog[d.pc];
+    if (a.is_compute()) {
+      for (cudaEvent_t e : d.pending) ck(cudaStreamWaitEvent(d.compute, e, 0), "wait arrival");
+      d.pending.clear();
+      d.last_start = next_event(d);
+      ck(cudaEventRecord(d.last_start, d.compute), "record start");
+      if (a.kind == ActionKind::Forward) forward(d, a);
+      else backward(d, a);
+      if (tracing_) {
+        cudaEvent_t e = next_event(d);
+        ck(cudaEventRecord(e, d.compute), "record end");
+        d.recs.push_back({static_cast<int>(d.pc), a.kind, a.microbatch, a.slice_index, d.last_start, e});
+      }
+    } else if (a.kind == ActionKind::OptimizerStep) {
+      optimizer(d);
+    } else if (transport_ == WP_TRANSPORT_NCCL) {
+      // One in-order NCCL stream per rank; BE = grouped send+recv (rendezvous-safe).
+      const MsgKey out = key_of(a);
+      auto recv_into = [&](const MsgKey& kin, int peer, size_t bytes) {
+        BufPtr landing = d.pool->alloc(bytes, d.copy, 1);
+        ckn(ncclRecv(landing->p, bytes, ncclUint8, peer, comm, d.copy), "ncclRecv");
+        d.inbox[kin] = landing;
+      };
+      const size_t msg_bytes = size_t(m_.tokens()) * m_.hidden * m_.act_bytes();
+      if (a.kind == ActionKind::Receive) {
+        ck(cudaStreamWaitEvent(d.copy, d.last_start ? d.last_start : d.step_begin, 0), "wait post");
+        recv_into(key_of(a), a.peer, msg_bytes);
+      } else {
+        auto it = d.outbox.find(out);
+        if (it == d.outbox.end()) throw wavepipe::SimulationError("runtime: send before its producer");
+        ck(cudaStreamWaitEvent(d.copy, d.outbox_ready[out], 0), "wait ready");
+        if (a.kind == ActionKind::BatchedExchange) ckn(ncclGroupStart(), "group");
+        ckn(ncclSend(it->second->p, msg_bytes, ncclUint8, a.peer, comm, d.copy), "ncclSend");
+        if (a.kind == ActionKind::BatchedExchange) {
+          const auto [q, qi] = d.be_partner[d.pc];
+          recv_into(key_of(list_.per_device[q][qi]), a.peer, msg_bytes);
+          ckn(ncclGroupEnd(), "group");
+        }
+        d.pool->release(it->second, d.copy);
+        d.outbox.erase(it);
+      }
+      if (a.kind != ActionKind::Send) {  // only incoming data gates the next compute
+        cudaEvent_t arrive = next_event(d);
+        ck(cudaEventRecord(arrive, d.copy), "record arrival");
+        d.pending.push_back(arrive);
+      }
+    } else {
+      // In-process transport.
+      auto publish = [&](const MsgKey& k) {
+        auto it = d.outbox.find(k);
+        if (it == d.outbox.end()) throw wavepipe::SimulationError("runtime: send before its producer");
+        published_[k] = Published{d.pipe, it->second, d.outbox_ready[k]};
+        d.outbox.erase(it);
+        d.outbox_ready.erase(k);
+      };
+      if (a.kind == ActionKind::Send) {
+        publish(key_of(a));
+      } else if (a.kind == ActionKind::Receive) {
+        auto it = published_.find(key_of(a));
+        if (it == published_.end()) break;  // sender has not produced it yet
+        Published msg = it->second;
+        published_.erase(it);
+        post_copy(d, key_of(a), msg);
+      } else {  // BatchedExchange
+        if (!d.published_at[d.pc]) {
+          publish(key_of(a));
+          d.published_at[d.pc] = 1;
+        }
+        const auto [q, qi] = d.be_partner[d.pc];
+        const MsgKey kin = key_of(list_.per_device[q][qi]);
+        auto it = published_.find(kin);
+        if (it == published_.end()) break;  // counterpart not at the exchange yet
+        Published msg = it->second;
+        published_.erase(it);
+        // An exchange has no prefetch anchor of its own: it moves as soon as
+        // both sides reach it (ref src/simulate.cpp:134-155).
+        cudaEvent_t saved = d.last_start;
+        d.last_start = d.step_begin;
+        post_copy(d, kin, msg);
+        d.last_start = saved;
+      }
+    }
+    ++d.pc;
+    moved = true;
+  }
+  return moved;
+}
+
+void Runtime::enqueue_step() {
+  for (bool moved = true; moved;) {
+    moved = false;
+    for (auto& d : devs_) moved = advance(*d) || moved;
+  }
+  for (auto& d : devs_) {
+    if (d->pc < list_.per_device[d->pipe].size()) {
+      throw wavepipe::SimulationError("runtime stalled: device " + std::to_string(d->pipe) + " blocked at " +
+                                      wavepipe::describe_action(list_.per_device[d->pipe][d->pc]));
+    }
+  }
+}
+
+float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_device) {
+  const size_t n = size_t(list_.config.microbatches) * m_.tokens();
+  for (auto& d : devs_) {
+    DevGuard g(d->cuda);
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    ck(cudaMemcpyAsync(d->tokens, tokens, n * sizeof(int32_t), on_device ? cudaMemcpyDefault : kind, d->compute),
+       "tokens H2D");
+    ck(cudaMemcpyAsync(d->labels, labels, n * sizeof(int32_t), on_device ? cudaMemcpyDefault : kind, d->compute),
+       "labels H2D");
+    ck(cudaMemsetAsync(d->loss, 0, sizeof(float), d->compute), "loss reset");
+    if (!update_) ck(cudaMemsetAsync(d->grad, 0, d->nparam * sizeof(float), d->compute), "grad reset");
+    d->pc = 0;
+    d->ev_next = 0;
+    d->pending.clear();
+    d->last_start = nullptr;
+    d->recs.clear();
+    d->comm_recs.clear();
+    d->published_at.assign(list_.per_device[d->pipe].size(), 0);
+    ck(cudaEventRecord(d->step_begin, d->compute), "record step begin");
+    ck(cudaStreamWaitEvent(d->copy, d->step_begin, 0), "copy after begin");
+  }
+  enqueue_step();
+  float loss = 0.f;
+  for (auto& d : devs_) {
+    DevGuard g(d->cuda);
+    ck(cudaStreamSynchronize(d->copy), "step sync");
+    ck(cudaStreamSynchronize(d->compute), "step sync");
+    float l = 0.f;
+    ck(cudaMemcpy(&l, d->loss, sizeof(float), cudaMemcpyDeviceToHost), "loss D2H");
+    loss += l;
+    if (!d->stash.empty() || !d->handoff.empty() || !d->inbox.empty() || !d->outbox.empty()) {
+      throw wavepipe::SimulationError("runtime: state left over at the end of the step");
+    }
+  }
+  if (tracing_) collect_trace();
+  ++step_;
+  return loss;
+}
+
+void Runtime::collect_trace() {
+  trace_ = wavepipe::SimTrace{};
+  trace_.intervals.resize(list_.config.devices);
+  auto rel = [](DeviceState* d, cudaEvent_t e) {
+    float ms = 0.f;
+    DevGuard g(d->cuda);
+    ck(cudaEventElapsedTime(&ms, d->step_begin, e), "event time");
+    return 1e-3 * ms;
+  };
+  for (auto& d : devs_) {
+    for (const auto& r : d->recs) {
+      wavepipe::TraceInterval iv;
+      iv.action_index = r.idx;
+      iv.kind = r.kind;
+      iv.microbatch = r.mb;
+      iv.slice_index = r.slice;
+      iv.direction = wavepipe::microbatch_direction(list_.config, r.mb);
+      iv.start = rel(d.get(), r.s);
+      iv.end = rel(d.get(), r.e);
+      trace_.makespan = std::max(trace_.makespan, iv.end);
+      trace_.intervals[d->pipe].push_back(iv);
+    }
+    for (const auto& c : d->comm_recs) {
+      wavepipe::CommEvent ev{c.src, c.dst, rel(c.post_dev, c.post), rel(c.arrive_dev, c.arrive)};
+      trace_.makespan = std::max(trace_.makespan, ev.arrival_time);
+      trace_.comm_events.push_back(ev);
+    }
+  }
+  std::sort(trace_.comm_events.begin(), trace_.comm_events.end(),
+            [](const wavepipe::CommEvent& x, const wavepipe::CommEvent& y) {
+              return std::tie(x.arrival_time, x.post_time, x.src_device, x.dst_device) <
+                     std::tie(y.arrival_time, y.post_time, y.src_device, y.dst_device);
+            });
+}
+
+// ------------------------------------------------------------- parameters
+const ParamDesc& Runtime::param_desc(int i, bool* owned) const {
+  const auto& ref = param_index_.at(param_names_.at(i));
+  if (owned) *owned = ref.device >= 0;
+  return ref.desc;
+}
+
+void Runtime::get_param(const std::string& name, float* host, int64_t n, bool want_grad) {
+  auto it = param_index_.find(name);
+  if (it == param_index_.end()) throw wavepipe::ConfigError("unknown or non-local parameter: " + name);
+  if (n != it->second.desc.numel) throw wavepipe::ConfigError("size mismatch for " + name);
+  DeviceState& d = *devs_[it->second.device];
+  DevGuard g(d.cuda);
+  ck(cudaDeviceSynchronize(), "sync");
+  const float* src = (want_grad ? d.grad : d.master) + d.params[it->second.slot].offset;
+  ck(cudaMemcpy(host, src, n * sizeof(float), cudaMemcpyDeviceToHost), "param D2H");
+}
+
+void Runtime::set_param(const std::string& name, const float* host, int64_t n) {
+  auto it = param_index_.find(name);
+  if (it == param_index_.end()) throw wavepipe::ConfigError("unknown or non-local parameter: " + name);
+  if (n != it->second.desc.numel) throw wavepipe::ConfigError("size mismatch for " + name);
+  DeviceState& d = *devs_[it->second.device];
+  DevGuard g(d.cuda);
+  ck(cudaDeviceSynchronize(), "sync");
+  const int64_t off = d.params[it->second.slot].offset;
+  ck(cudaMemcpy(d.master + off, host, n * sizeof(float), cudaMemcpyHostToDevice), "param H2D");
+  if (d.shadow) {
+    launches_ += wpk::cast_f32_to_bf16(d.master + off, static_cast<__nv_bfloat16*>(d.shadow) + off, n, d.compute);
+    ck(cudaStreamSynchronize(d.compute), "sync");
+  }
+}
+
+}  // namespace wprt

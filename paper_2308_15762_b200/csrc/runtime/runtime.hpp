@@ -1,0 +1,159 @@
+// GPU executor of a wavepipe ActionList.
+//
+// The reference executes lists only in abstract time (src/simulate.cpp:57-178);
+// this runtime keeps that contract on real hardware:
+//   Forward/Backward  kernels of the slice at local_module_rank on the device's
+//                     compute stream; the stash slot of (microbatch, slice) lives
+//                     from forward start to backward end (src/analytics.cpp:61-76)
+//   Send              buffered: the producer's output is published with a ready
+//                     event; nothing blocks the compute stream (:117-122)
+//   Receive           the copy is *posted* at the start of the preceding compute
+//                     (depth-1 prefetch, :123-133) and its arrival gates only the
+//                     next compute
+//   BatchedExchange   both directions of the pair move as one exchange; the
+//                     incoming message is the counterpart's outgoing one (:134-155)
+//   OptimizerStep     fused optimizer over the device's parameters (flush)
+// Copies run on the *sender's* copy stream (push over NVLink / peer DMA, or
+// D2D when several pipeline devices share one GPU), gated by the receiver's
+// post event, so a message never lands before the receiver would have posted
+// it -- the reference's memory bound holds.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kernels/gemm.cuh"
+#include "kernels/ops.cuh"
+#include "runtime/model.hpp"
+#include "wavepipe/core.hpp"
+
+namespace wprt {
+
+// One device allocation from a per-device pool.  Message buffers (landing
+// and outbox) carry an event recorded at free time so the next user on a
+// different stream waits for the last one.
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int pool_class = 0;  // 0 compute-only, 1 message
+  cudaEvent_t ev = nullptr;
+  bool ev_pending = false;
+};
+using BufPtr = std::shared_ptr<Buf>;
+
+class Pool {
+ public:
+  Pool(int cuda_dev, cudaStream_t home) : dev_(cuda_dev), home_(home) {}
+  ~Pool();
+  BufPtr alloc(size_t bytes, cudaStream_t stream, int pool_class);
+  void release(const BufPtr& b, cudaStream_t stream);
+  size_t reserved() const { return reserved_; }
+
+ private:
+  int dev_;
+  cudaStream_t home_;
+  std::map<std::pair<int, size_t>, std::vector<BufPtr>> free_;
+  std::vector<BufPtr> all_;
+  size_t reserved_ = 0;
+};
+
+// Saved tensors of one unit for its backward.
+struct UnitStash {
+  BufPtr x, ln, mean, rstd, a, b, c;  // attn: a=qkv b=P c=ctx; mlp: a=u b=g; head: a=dlogits
+};
+
+struct SliceStash {
+  std::vector<UnitStash> units;  // in unit order of the slice
+};
+
+struct MsgKey {
+  int payload, mb, low;
+  bool operator<(const MsgKey& o) const {
+    return payload != o.payload ? payload < o.payload : mb != o.mb ? mb < o.mb : low < o.low;
+  }
+};
+
+struct Published {
+  int src = -1;
+  BufPtr buf;
+  cudaEvent_t ready = nullptr;
+};
+
+struct ParamSlot {
+  ParamDesc desc;
+  int64_t offset = 0;  // element offset in the device's flat buffers
+};
+
+struct DeviceState;
+
+class Runtime {
+ public:
+  Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, int transport, const int* device_ids,
+          int rank, const void* nccl_id);
+  ~Runtime();
+
+  float train_step(const int32_t* tokens, const int32_t* labels, bool on_device);
+
+  const wavepipe::SimTrace& trace() const { return trace_; }
+  void set_tracing(bool on) { tracing_ = on; }
+  void set_update(bool on) { update_ = on; }
+  int64_t launches() const { return launches_; }
+
+  int param_count() const { return static_cast<int>(param_index_.size()); }
+  const ParamDesc& param_desc(int i, bool* owned) const;
+  void get_param(const std::string& name, float* host, int64_t n, bool grad);
+  void set_param(const std::string& name, const float* host, int64_t n);
+
+ private:
+  struct ParamRef {
+    int device;  // local device index owning it (-1: other process)
+    int slot;
+    ParamDesc desc;
+  };
+
+  void build_devices(const int* device_ids);
+  void init_params(DeviceState& d);
+  void enqueue_step();
+  bool advance(DeviceState& d);
+  void forward(DeviceState& d, const wavepipe::Action& a);
+  void backward(DeviceState& d, const wavepipe::Action& a);
+  void optimizer(DeviceState& d);
+  void post_copy(DeviceState& dst, const MsgKey& key, Published msg);
+  BufPtr take_input(DeviceState& d, const MsgKey& key);
+  void deliver(DeviceState& d, const MsgKey& key, BufPtr buf);
+  cudaEvent_t next_event(DeviceState& d);
+  void collect_trace();
+  int owner_device(int mb, int slice) const;
+
+  // unit kernels
+  BufPtr unit_fwd(DeviceState& d, int unit, int mb, BufPtr x, UnitStash& st);
+  BufPtr unit_bwd(DeviceState& d, int unit, int mb, UnitStash& st, BufPtr dy);
+  void gemm(DeviceState& d, const wpk::GemmProblem& g);
+  const void* weight(DeviceState& d, const std::string& name) const;  // act dtype (shadow or master)
+  float* master(DeviceState& d, const std::string& name) const;
+  float* grad(DeviceState& d, const std::string& name) const;
+
+  ModelSpec m_;
+  wavepipe::ActionList list_;
+  std::vector<Unit> units_;
+  std::vector<int> bounds_;  // slice -> unit range
+  int transport_;
+  int rank_;
+  std::vector<std::unique_ptr<DeviceState>> devs_;  // local pipeline devices
+  std::vector<int> dev_of_pipeline_;                // pipeline device -> index in devs_ (-1 remote)
+  std::unordered_map<std::string, ParamRef> param_index_;
+  std::vector<std::string> param_names_;
+  std::map<MsgKey, Published> published_;
+  bool tracing_ = false, update_ = true;
+  int step_ = 0;
+  int64_t launches_ = 0;
+  wavepipe::SimTrace trace_;
+  void* nccl_comm_ = nullptr;
+};
+
+}  // namespace wprt

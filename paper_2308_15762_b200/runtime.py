@@ -1,0 +1,145 @@
+"""GPU train-step runtime: executes a wavepipe ActionList on B200s.
+
+Python face of `wp_runtime_*` / `wp_train_step` in include/wavepipe.h.  The
+C++ runtime drives CUDA streams/events and the sm_100a kernels; this module
+only marshals arguments.  There is no CPU fallback: creating a Runtime
+without a CUDA device raises CudaError.
+"""
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._native import check, lib, wp_model_desc
+from .schedule import ActionList, SimTrace
+
+TRANSPORT_LOCAL = 0
+TRANSPORT_NCCL = 1
+
+
+@dataclass
+class ModelDesc:
+    """ModelSpec of the stage compute (GPT-like causal LM or BERT-like)."""
+    layers: int = 4
+    hidden: int = 256
+    heads: int = 4
+    ffn: int = 1024
+    seq: int = 128
+    vocab: int = 1024
+    micro_batch_size: int = 2
+    causal: bool = True
+    tie_embeddings: bool = True
+    dtype: str = "fp32"          # "fp32" (parity mode) or "bf16"
+    optimizer: str = "sgd"       # "sgd" or "adamw"
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.95
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+    seed: int = 1234
+
+    def _c(self):
+        return wp_model_desc(self.layers, self.hidden, self.heads, self.ffn, self.seq, self.vocab,
+                             self.micro_batch_size, int(self.causal), int(self.tie_embeddings),
+                             0 if self.dtype == "fp32" else 1, 0 if self.optimizer == "sgd" else 1,
+                             self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, self.seed)
+
+    @property
+    def tokens_per_microbatch(self):
+        return self.micro_batch_size * self.seq
+
+    def flops_per_sample(self):
+        """3 x forward FLOPs: L*(2*(4h^2+2hf) + a*s*h) + 2hV per token."""
+        a = 2 if self.causal else 4
+        h, f, s = self.hidden, self.ffn, self.seq
+        per_token = self.layers * (2 * (4 * h * h + 2 * h * f) + a * s * h) + 2 * h * self.vocab
+        return 3.0 * s * per_token
+
+
+class Runtime:
+    def __init__(self, model: ModelDesc, schedule: ActionList, transport=TRANSPORT_LOCAL, device_ids=None,
+                 rank=0, nccl_id=None):
+        self.model = model
+        self.schedule = schedule
+        P = schedule.config.devices
+        n_ids = P if transport == TRANSPORT_LOCAL else 1
+        ids = list(device_ids) if device_ids is not None else [0] * n_ids
+        self._ids = (C.c_int * len(ids))(*ids)
+        self._desc = model._c()
+        nid = None
+        if nccl_id is not None:
+            self._nccl = C.create_string_buffer(bytes(nccl_id), 128)
+            nid = C.cast(self._nccl, C.c_void_p)
+        h = C.c_void_p()
+        check(lib.wp_runtime_create(C.byref(self._desc), schedule.handle, transport, self._ids, rank, nid,
+                                    C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.wp_runtime_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    # --------------------------------------------------------------- steps
+    def train_step(self, tokens, labels):
+        """One synchronous step over all microbatches.  tokens/labels: int32
+        [B, micro_batch_size, seq] as numpy arrays (host) or CUDA tensors
+        (device).  Returns the mean loss over microbatches."""
+        on_dev = 0
+        if hasattr(tokens, "is_cuda"):
+            on_dev = int(tokens.is_cuda)
+            tp, lp = tokens.data_ptr(), labels.data_ptr()
+        else:
+            tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+            labels = np.ascontiguousarray(labels, dtype=np.int32)
+            tp, lp = tokens.ctypes.data, labels.ctypes.data
+        loss = C.c_float()
+        check(lib.wp_train_step(self._h, C.c_void_p(tp), C.c_void_p(lp), on_dev, C.byref(loss)))
+        return loss.value
+
+    def set_tracing(self, on=True):
+        check(lib.wp_runtime_set_tracing(self._h, int(on)))
+
+    def set_update(self, on=True):
+        check(lib.wp_runtime_set_update(self._h, int(on)))
+
+    def trace(self) -> SimTrace:
+        """Measured trace of the last traced step (seconds)."""
+        p = C.c_void_p()
+        check(lib.wp_runtime_trace(self._h, C.byref(p)))
+        return SimTrace(p, owned=False)
+
+    def launch_count(self):
+        n = C.c_int64()
+        check(lib.wp_runtime_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    # ----------------------------------------------------------- parameters
+    def param_names(self):
+        n = C.c_int()
+        check(lib.wp_param_count(self._h, C.byref(n)))
+        out = []
+        for i in range(n.value):
+            name = C.c_char_p()
+            numel = C.c_int64()
+            owned = C.c_int()
+            check(lib.wp_param_info(self._h, i, C.byref(name), C.byref(numel), C.byref(owned)))
+            out.append((name.value.decode(), numel.value))
+        return out
+
+    def get_param(self, name, numel):
+        buf = np.empty(numel, dtype=np.float32)
+        check(lib.wp_get_param(self._h, name.encode(), buf.ctypes.data_as(C.POINTER(C.c_float)), numel))
+        return buf
+
+    def get_grad(self, name, numel):
+        buf = np.empty(numel, dtype=np.float32)
+        check(lib.wp_get_grad(self._h, name.encode(), buf.ctypes.data_as(C.POINTER(C.c_float)), numel))
+        return buf
+
+    def set_param(self, name, values):
+        arr = np.ascontiguousarray(values, dtype=np.float32).ravel()
+        check(lib.wp_set_param(self._h, name.encode(), arr.ctypes.data_as(C.POINTER(C.c_float)), arr.size))
