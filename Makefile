@@ -32,7 +32,7 @@ $(OBJ)/%.cu.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
 
 $(LIB): $(CORE_OBJS) $(CU_OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(CUDA)/lib64 -lcudart_static -lnccl -ldl -lpthread -lrt
+	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(CUDA)/lib64 -lcudart_static -ldl -lpthread -lrt
 
 oracle:
 	$(MAKE) -C oracle

@@ -1,0 +1,339 @@
+"""Benchmark: Hanayo wave-pipeline training step on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl wavepipe|reference]
+
+Workload (BASELINE.json configs[3]): GPT-1.3B-like (24 layers, hidden 2048,
+16 heads, ffn 8192, seq 1024, vocab 50304, tied embeddings), bf16 tensor-core
+compute with fp32 master weights and AdamW, Hanayo W=2 over P=N GPUs
+(N=1: all S=4 slices resident on one GPU), B=8 microbatches of 4 sequences,
+synthetic tokens (splitmix64), random-init weights.
+
+One "step" = one full synchronous training iteration: every microbatch's
+forward and backward through every slice, the flush, and the optimizer
+update.  `value` is samples/s with inputs resident in HBM; `e2e` is the same
+step through the public API with the token/label batch copied from pinned
+host memory every step and the loss read back.  The per-step working set
+(~35 GB of weights, optimizer state and activations) is far larger than the
+126 MB L2, so no explicit flush is needed between steps.
+
+Multi-GPU (torchrun, one rank per GPU): NCCL transport, rank r = pipeline
+device r; fixed global batch (strong scaling); time = max over ranks.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+GPT13B = dict(layers=24, hidden=2048, heads=16, ffn=8192, seq=1024, vocab=50304)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def model_desc(args):
+    import paper_2308_15762_b200 as wp
+    return wp.ModelDesc(**GPT13B, micro_batch_size=args.mbs, causal=True, tie_embeddings=True, dtype="bf16",
+                        optimizer="adamw", lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.01, seed=1234)
+
+
+def cpu_port_sample(desc, threads=None):
+    """Time the oracle's torch-CPU fp32 train step on a bounded sample: one
+    sequence through (embedding + 1 transformer layer + LM head) at the full
+    hidden/ffn/seq/vocab, forward+backward; extrapolate to samples/s of the
+    full model by FLOPs (work conservation, proj/tests/test_simulate.cpp:67-79)."""
+    import torch
+    from oracle import model as om
+    from paper_2308_15762_b200.data import synthetic_batch
+    threads = threads or os.cpu_count()
+    torch.set_num_threads(threads)
+
+    class D:
+        pass
+
+    d1 = D()
+    for k in ("layers", "hidden", "heads", "ffn", "seq", "vocab", "micro_batch_size", "causal",
+              "tie_embeddings"):
+        setattr(d1, k, getattr(desc, k))
+    d1.layers, d1.micro_batch_size = 1, 1
+    params = om.init_params(d1, seed=1, nonzero_vectors=False)
+    tok, lab = synthetic_batch(1, 1, d1.seq, d1.vocab)
+    t0 = time.perf_counter()
+    om.reference_step(params, tok, lab, d1, dtype=torch.float32)
+    dt = time.perf_counter() - t0
+    a = 2 if desc.causal else 4
+    h, f, s = desc.hidden, desc.ffn, desc.seq
+    reduced = 3.0 * s * ((2 * (4 * h * h + 2 * h * f) + a * s * h) + 2 * h * desc.vocab)
+    rate = reduced / dt
+    return rate / desc.flops_per_sample(), dt, threads
+
+
+def ref_schedule_time(P, B, W):
+    """The reference's own CPU path (oracle/_ref: its src/*.cpp, generate +
+    simulate), single-threaded as the reference is."""
+    drv = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+    if not os.path.exists(drv):
+        return None
+    out = subprocess.run([drv, "time", "hanayo", str(P), str(B), str(W), "5"], capture_output=True, text=True)
+    try:
+        return json.loads(out.stdout)["best_ms"]
+    except (ValueError, KeyError):
+        return None
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the reference's CPU implementation of the path, timed on
+    this box's host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    desc = model_desc(args)
+    for _ in range(args.warmup):
+        cpu_port_sample(desc)
+    vals, per = [], []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, dt, cores = cpu_port_sample(desc)
+        vals.append(v)
+        per.append(dt)
+    wall = time.perf_counter() - t0
+    value = statistics.median(vals)
+    ref_ms = ref_schedule_time(args.gpus, args.microbatches, args.waves)
+    sample = (f"1 sequence x (embedding + 1 of 24 layers + LM head) of GPT-1.3B, fp32 torch CPU "
+              f"fwd+bwd ({statistics.median(per):.2f} s), extrapolated to the full model by FLOPs; "
+              f"schedule generate+simulate by the reference's own code (oracle/_ref): "
+              f"{ref_ms if ref_ms is not None else 'n/a'} ms")
+    line = {
+        "impl": "reference", "metric": "samples/sec (Hanayo W=2 train step)", "value": value,
+        "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic tokens (splitmix64), random-init weights",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world):
+    return {"workload": "GPT-1.3B-like train step, Hanayo W=%d over P=%d" % (args.waves, world),
+            "model": "gpt-1.3b-like", "layers": 24, "hidden": 2048, "heads": 16, "ffn": 8192, "seq_len": 1024,
+            "vocab": 50304, "micro_batch_size": args.mbs, "microbatches": args.microbatches,
+            "global_batch": args.mbs * args.microbatches, "schedule": f"hanayo P={world} W={args.waves} "
+            f"B={args.microbatches}", "parallelism": f"pp{world}", "optimizer": "adamw",
+            "l2_flush": "not needed: per-step working set (~35 GB) >> 126 MB L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="wavepipe", choices=["wavepipe", "reference"])
+    ap.add_argument("--microbatches", type=int, default=8)
+    ap.add_argument("--mbs", type=int, default=4)
+    ap.add_argument("--waves", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2308_15762_b200 as wp
+    from paper_2308_15762_b200.data import synthetic_batch
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    args.gpus = world
+    desc = model_desc(args)
+    cfg = wp.make_config(wp.Scheme.Hanayo, world, args.microbatches, args.waves)
+    sched = wp.generate_schedule(cfg)
+    if world > 1:
+        obj = [wp.runtime.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_NCCL, device_ids=[local_rank], rank=rank,
+                        nccl_id=obj[0])
+    else:
+        rt = wp.Runtime(desc, sched, device_ids=[local_rank])
+
+    tok_np, lab_np = synthetic_batch(args.microbatches, args.mbs, desc.seq, desc.vocab)
+    tok_d = torch.from_numpy(tok_np).cuda()
+    lab_d = torch.from_numpy(lab_np).cuda()
+    tok_h = torch.from_numpy(tok_np).pin_memory()
+    lab_h = torch.from_numpy(lab_np).pin_memory()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(steps, host):
+        barrier()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        loss = None
+        for _ in range(steps):
+            loss = rt.train_step(tok_h, lab_h) if host else rt.train_step(tok_d, lab_d)
+        en.record()
+        barrier()
+        sec = st.elapsed_time(en) / 1e3
+        if world > 1:
+            t = torch.tensor([sec], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sec = float(t.item())
+        return sec, loss
+
+    for _ in range(args.warmup):
+        rt.train_step(tok_d, lab_d)
+
+    # Device-resident timed region (value), with GEMM profiling and clocks.
+    rt.set_profiling(True)
+    launches0 = rt.launch_count()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    sec, loss = timed(args.steps, host=False)
+    clk = clocks.stop()
+    launches = rt.launch_count() - launches0
+    g_launches, g_flops, g_sec = rt.gemm_stats()
+    rt.set_profiling(False)
+
+    # End-to-end through the public API from pinned host buffers.
+    sec_e2e, _ = timed(args.steps, host=True)
+
+    # One traced step: measured vs simulated bubble.
+    rt.set_tracing(True)
+    rt.train_step(tok_d, lab_d)
+    rt.set_tracing(False)
+    tr = rt.trace()
+    measured_bubble = wp.bubble_ratio(tr)
+    fwd = [iv.end - iv.start for dev in tr.intervals for iv in dev if iv.kind == wp.ActionKind.Forward]
+    bwd = [iv.end - iv.start for dev in tr.intervals for iv in dev if iv.kind == wp.ActionKind.Backward]
+    tf, tb = statistics.mean(fwd) * 2 * args.waves, statistics.mean(bwd) * 2 * args.waves
+    sim = wp.simulate(sched, wp.CostModel(tf, tb, 0.0))
+    sim_bubble = wp.bubble_ratio(sim)
+    eq1 = wp.analytic_bubble_hanayo_d(world, args.waves, tf, tb, 0.0) if world >= 2 else None
+
+    if rank != 0:
+        return
+    samples = args.microbatches * args.mbs * args.steps
+    value = samples / sec
+    peaks, peaks_kind = load_peaks()
+    peak_tc = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
+    achieved = g_flops / g_sec / 1e12 if g_sec > 0 else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    except OSError:
+        pass
+    flops_step = desc.flops_per_sample() * args.microbatches * args.mbs
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, dt, cores = cpu_port_sample(desc)
+        cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
+               "sample": f"1 sequence x (embedding + 1 of 24 layers + LM head), fp32 torch CPU fwd+bwd "
+                         f"({dt:.2f} s), extrapolated to the 24-layer model by FLOPs"}
+    line = {
+        "metric": "samples/sec (Hanayo W=2 train step)", "value": value, "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic tokens (splitmix64), random-init weights",
+        "config": workload_config(args, world),
+        "tc_peak_frac": flops_step * args.steps / sec / world / (peak_tc * 1e12),
+        "bubble": {"measured": measured_bubble, "simulated_at_measured_costs": sim_bubble, "eq1": eq1,
+                   "t_forward_s": tf, "t_backward_s": tb},
+        "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05, all GEMM launches of the step)",
+                     "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
+                     "frac": achieved / peak_tc if achieved else None, "traffic": traffic,
+                     "peak_kind": f"{peaks_kind} bf16 sustained (kernel timed inside a long step)",
+                     "gemm_launches": g_launches, "gemm_share_of_step": g_sec / (sec * 1.0)},
+        "cpu_baseline": cpu,
+        "e2e": {"value": samples / sec_e2e, "unit": "samples/s",
+                "h2d_bytes_per_step": int(tok_h.numel() * 4 + lab_h.numel() * 4), "d2h_bytes_per_step": 4},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "loss": loss,
+    }
+    print(json.dumps(line), flush=True)
+    rt.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

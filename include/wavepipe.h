@@ -156,6 +156,8 @@ int wp_runtime_create(const wp_model_desc* model, const wp_list* list, int trans
                       const int* device_ids, int rank, const void* nccl_id,
                       wp_runtime** out);
 void wp_runtime_free(wp_runtime* rt);
+/* ncclGetUniqueId for rank 0 of a WP_TRANSPORT_NCCL job (128 bytes). */
+int wp_nccl_unique_id(void* out128);
 
 /* One synchronous training step (all microbatches, flush, optimizer).
  * tokens/labels: int32 [B * micro_batch_size * seq], microbatch-major, in HOST
@@ -178,8 +180,12 @@ int wp_get_param(wp_runtime* rt, const char* name, float* host_out, int64_t nume
 int wp_set_param(wp_runtime* rt, const char* name, const float* host_in, int64_t numel);
 int wp_get_grad(wp_runtime* rt, const char* name, float* host_out, int64_t numel);
 
-/* Number of this library's kernels launched by the last train step. */
+/* Number of this library's kernels launched since the runtime was created. */
 int wp_runtime_launch_count(const wp_runtime* rt, int64_t* launches);
+/* GEMM profiling: CUDA events around every tcgen05/SIMT GEMM launch on its
+ * own stream, accumulated over the steps run while enabled (enabling resets). */
+int wp_runtime_set_profiling(wp_runtime* rt, int enabled);
+int wp_runtime_gemm_stats(const wp_runtime* rt, int64_t* launches, double* flops, double* seconds);
 
 #ifdef __cplusplus
 }

@@ -90,6 +90,7 @@ _SIGS = {
     "wp_analytic_bubble_simplified": (I, [I, I, I64P]),
     "wp_runtime_create": (I, [C.POINTER(wp_model_desc), P, I, IP, I, C.c_void_p, PP]),
     "wp_runtime_free": (None, [P]),
+    "wp_nccl_unique_id": (I, [C.c_void_p]),
     "wp_train_step": (I, [P, C.c_void_p, C.c_void_p, I, C.POINTER(C.c_float)]),
     "wp_runtime_trace": (I, [P, PP]),
     "wp_runtime_set_tracing": (I, [P, I]),
@@ -100,6 +101,8 @@ _SIGS = {
     "wp_set_param": (I, [P, C.c_char_p, C.POINTER(C.c_float), C.c_int64]),
     "wp_get_grad": (I, [P, C.c_char_p, C.POINTER(C.c_float), C.c_int64]),
     "wp_runtime_launch_count": (I, [P, I64P]),
+    "wp_runtime_set_profiling": (I, [P, I]),
+    "wp_runtime_gemm_stats": (I, [P, I64P, DP, DP]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,9 +1,12 @@
 // C ABI of the GPU runtime (include/wavepipe.h, "GPU runtime" section).
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include <memory>
 
 #include "capi_internal.hpp"
+#include "runtime/nccl_shim.hpp"
 #include "runtime/runtime.hpp"
 
 struct wp_runtime {
@@ -40,6 +43,21 @@ int wp_runtime_create(const wp_model_desc* model, const wp_list* list, int trans
 }
 
 void wp_runtime_free(wp_runtime* rt) { delete rt; }
+
+int wp_nccl_unique_id(void* out128) {
+  if (!out128) return fail(WP_ERR_CONFIG, "null argument");
+  ncclUniqueId id;
+  try {
+    const auto& api = wprt::NcclApi::get();
+    const ncclResult_t r = api.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(WP_ERR_CUDA, std::string("ncclGetUniqueId: ") + api.GetErrorString(r));
+  } catch (const std::exception& e) {
+    return fail(WP_ERR_CUDA, e.what());
+  }
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, sizeof(id));
+  return WP_OK;
+}
 
 int wp_train_step(wp_runtime* rt, const int32_t* tokens, const int32_t* labels, int on_device, float* loss) {
   try {
@@ -120,6 +138,19 @@ int wp_get_grad(wp_runtime* rt, const char* name, float* host_out, int64_t numel
   } catch (...) {
     return map_exception();
   }
+}
+
+int wp_runtime_set_profiling(wp_runtime* rt, int enabled) {
+  if (!rt) return fail(WP_ERR_CONFIG, "null argument");
+  rt->rt->set_profiling(enabled != 0);
+  if (enabled) rt->rt->reset_gemm_stats();
+  return WP_OK;
+}
+
+int wp_runtime_gemm_stats(const wp_runtime* rt, int64_t* launches, double* flops, double* seconds) {
+  if (!rt || !launches || !flops || !seconds) return fail(WP_ERR_CONFIG, "null argument");
+  rt->rt->gemm_stats(launches, flops, seconds);
+  return WP_OK;
 }
 
 int wp_runtime_launch_count(const wp_runtime* rt, int64_t* launches) {

@@ -1,7 +1,6 @@
 // Runtime: parameters, stash pools and the per-device action interpreter.
 // See runtime.hpp for the executor contract and its reference citations.
 #include <cuda_bf16.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -10,6 +9,7 @@
 #include <stdexcept>
 
 #include "capi_internal.hpp"
+#include "runtime/nccl_shim.hpp"
 #include "runtime/runtime.hpp"
 
 namespace wprt {
@@ -23,7 +23,7 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw wpc::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 void ckn(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) throw wpc::CudaError(std::string(what) + ": " + ncclGetErrorString(r));
+  if (r != ncclSuccess) throw wpc::CudaError(std::string(what) + ": " + NcclApi::get().GetErrorString(r));
 }
 
 struct DevGuard {
@@ -141,6 +141,11 @@ struct DeviceState {
   };
   std::vector<Rec> recs;
   std::vector<CommRec> comm_recs;
+  struct GemmRec {
+    double flops;
+    cudaEvent_t s, e;
+  };
+  std::vector<GemmRec> gemm_recs;
 };
 
 // ------------------------------------------------------------------ runtime
@@ -170,13 +175,13 @@ Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, in
     std::memcpy(&id, nccl_id, sizeof(id));
     DevGuard g(devs_[0]->cuda);
     ncclComm_t comm;
-    ckn(ncclCommInitRank(&comm, P, id, rank_), "ncclCommInitRank");
+    ckn(NcclApi::get().CommInitRank(&comm, P, id, rank_), "ncclCommInitRank");
     nccl_comm_ = comm;
   }
 }
 
 Runtime::~Runtime() {
-  if (nccl_comm_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_comm_));
+  if (nccl_comm_) NcclApi::get().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
   for (auto& d : devs_) {
     DevGuard g(d->cuda);
     cudaDeviceSynchronize();
@@ -309,7 +314,17 @@ float* Runtime::grad(DeviceState& d, const std::string& name) const {
   return d.grad + d.params[it->second].offset;
 }
 
-void Runtime::gemm(DeviceState& d, const wpk::GemmProblem& g) { launches_ += wpk::gemm(g, d.compute); }
+void Runtime::gemm(DeviceState& d, const wpk::GemmProblem& g) {
+  if (!profiling_) {
+    launches_ += wpk::gemm(g, d.compute);
+    return;
+  }
+  cudaEvent_t s = next_event(d), e = next_event(d);
+  ck(cudaEventRecord(s, d.compute), "record gemm start");
+  launches_ += wpk::gemm(g, d.compute);
+  ck(cudaEventRecord(e, d.compute), "record gemm end");
+  d.gemm_recs.push_back({2.0 * g.M * g.N * g.K * g.nb1 * g.nb2, s, e});
+}
 
 cudaEvent_t Runtime::next_event(DeviceState& d) {
   if (d.ev_next == d.events.size()) {
@@ -667,7 +682,7 @@ bool Runtime::advance(DeviceState& d) {
       const MsgKey out = key_of(a);
       auto recv_into = [&](const MsgKey& kin, int peer, size_t bytes) {
         BufPtr landing = d.pool->alloc(bytes, d.copy, 1);
-        ckn(ncclRecv(landing->p, bytes, ncclUint8, peer, comm, d.copy), "ncclRecv");
+        ckn(NcclApi::get().Recv(landing->p, bytes, ncclUint8, peer, comm, d.copy), "ncclRecv");
         d.inbox[kin] = landing;
       };
       const size_t msg_bytes = size_t(m_.tokens()) * m_.hidden * m_.act_bytes();
@@ -678,12 +693,12 @@ bool Runtime::advance(DeviceState& d) {
         auto it = d.outbox.find(out);
         if (it == d.outbox.end()) throw wavepipe::SimulationError("runtime: send before its producer");
         ck(cudaStreamWaitEvent(d.copy, d.outbox_ready[out], 0), "wait ready");
-        if (a.kind == ActionKind::BatchedExchange) ckn(ncclGroupStart(), "group");
-        ckn(ncclSend(it->second->p, msg_bytes, ncclUint8, a.peer, comm, d.copy), "ncclSend");
+        if (a.kind == ActionKind::BatchedExchange) ckn(NcclApi::get().GroupStart(), "group");
+        ckn(NcclApi::get().Send(it->second->p, msg_bytes, ncclUint8, a.peer, comm, d.copy), "ncclSend");
         if (a.kind == ActionKind::BatchedExchange) {
           const auto [q, qi] = d.be_partner[d.pc];
           recv_into(key_of(list_.per_device[q][qi]), a.peer, msg_bytes);
-          ckn(ncclGroupEnd(), "group");
+          ckn(NcclApi::get().GroupEnd(), "group");
         }
         d.pool->release(it->second, d.copy);
         d.outbox.erase(it);
@@ -765,6 +780,7 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     d->last_start = nullptr;
     d->recs.clear();
     d->comm_recs.clear();
+    d->gemm_recs.clear();
     d->published_at.assign(list_.per_device[d->pipe].size(), 0);
     ck(cudaEventRecord(d->step_begin, d->compute), "record step begin");
     ck(cudaStreamWaitEvent(d->copy, d->step_begin, 0), "copy after begin");
@@ -783,6 +799,16 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     }
   }
   if (tracing_) collect_trace();
+  for (auto& d : devs_) {
+    DevGuard g(d->cuda);
+    for (const auto& r : d->gemm_recs) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, r.s, r.e), "gemm time");
+      prof_seconds_ += 1e-3 * ms;
+      prof_flops_ += r.flops;
+      ++prof_launches_;
+    }
+  }
   ++step_;
   return loss;
 }

@@ -1,0 +1,58 @@
+// Lazily-bound NCCL entry points.  libwavepipe.so does not link NCCL: the
+// host process usually already carries one (torch bundles its own
+// libnccl.so.2), and two different libnccl.so.2 builds in one process clash
+// at symbol resolution.  The NCCL transport binds to the already-loaded copy
+// (RTLD_NOLOAD) and only falls back to dlopen("libnccl.so.2") when none is
+// loaded yet.
+#pragma once
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+namespace wprt {
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+  static const NcclApi& get() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string error;
+    std::call_once(once, [] {
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+      if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) {
+        error = std::string("cannot load libnccl.so.2: ") + dlerror();
+        return;
+      }
+      auto sym = [&](const char* n) {
+        void* p = dlsym(h, n);
+        if (!p) error = std::string("libnccl.so.2 lacks ") + n;
+        return p;
+      };
+      api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+      api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+      api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+      api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+      api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+      api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+      api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+      api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    });
+    if (!error.empty()) throw std::runtime_error(error);
+    return api;
+  }
+};
+
+}  // namespace wprt

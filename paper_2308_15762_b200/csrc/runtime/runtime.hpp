@@ -102,6 +102,16 @@ class Runtime {
   const wavepipe::SimTrace& trace() const { return trace_; }
   void set_tracing(bool on) { tracing_ = on; }
   void set_update(bool on) { update_ = on; }
+  // Per-GEMM CUDA events on the launching (compute) stream; accumulated over
+  // the steps run while enabled: launches, executed FLOPs (2MNK per problem)
+  // and summed kernel time.
+  void set_profiling(bool on) { profiling_ = on; }
+  void gemm_stats(int64_t* launches, double* flops, double* seconds) const {
+    *launches = prof_launches_;
+    *flops = prof_flops_;
+    *seconds = prof_seconds_;
+  }
+  void reset_gemm_stats() { prof_launches_ = 0, prof_flops_ = 0, prof_seconds_ = 0; }
   int64_t launches() const { return launches_; }
 
   int param_count() const { return static_cast<int>(param_index_.size()); }
@@ -149,7 +159,9 @@ class Runtime {
   std::unordered_map<std::string, ParamRef> param_index_;
   std::vector<std::string> param_names_;
   std::map<MsgKey, Published> published_;
-  bool tracing_ = false, update_ = true;
+  bool tracing_ = false, update_ = true, profiling_ = false;
+  int64_t prof_launches_ = 0;
+  double prof_flops_ = 0, prof_seconds_ = 0;
   int step_ = 0;
   int64_t launches_ = 0;
   wavepipe::SimTrace trace_;

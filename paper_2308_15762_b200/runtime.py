@@ -56,6 +56,13 @@ class ModelDesc:
         return 3.0 * s * per_token
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it and broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    check(lib.wp_nccl_unique_id(buf))
+    return buf.raw
+
+
 class Runtime:
     def __init__(self, model: ModelDesc, schedule: ActionList, transport=TRANSPORT_LOCAL, device_ids=None,
                  rank=0, nccl_id=None):
@@ -116,6 +123,16 @@ class Runtime:
         n = C.c_int64()
         check(lib.wp_runtime_launch_count(self._h, C.byref(n)))
         return n.value
+
+    def set_profiling(self, on=True):
+        check(lib.wp_runtime_set_profiling(self._h, int(on)))
+
+    def gemm_stats(self):
+        """(launches, executed FLOPs, summed kernel seconds) of the GEMMs run
+        while profiling was enabled."""
+        n, fl, sec = C.c_int64(), C.c_double(), C.c_double()
+        check(lib.wp_runtime_gemm_stats(self._h, C.byref(n), C.byref(fl), C.byref(sec)))
+        return n.value, fl.value, sec.value
 
     # ----------------------------------------------------------- parameters
     def param_names(self):
