@@ -200,6 +200,7 @@ def main():
     ap.add_argument("--mbs", type=int, default=4)
     ap.add_argument("--waves", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gemm-report", action="store_true", help="per-shape GEMM table on stderr")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -270,6 +271,8 @@ def main():
     clk = clocks.stop()
     launches = rt.launch_count() - launches0
     g_launches, g_flops, g_sec = rt.gemm_stats()
+    if args.gemm_report and rank == 0:
+        print(rt.gemm_report(), file=sys.stderr, flush=True)
     rt.set_profiling(False)
 
     # End-to-end through the public API from pinned host buffers.

@@ -186,6 +186,8 @@ int wp_runtime_launch_count(const wp_runtime* rt, int64_t* launches);
  * own stream, accumulated over the steps run while enabled (enabling resets). */
 int wp_runtime_set_profiling(wp_runtime* rt, int enabled);
 int wp_runtime_gemm_stats(const wp_runtime* rt, int64_t* launches, double* flops, double* seconds);
+/* Text table of the profiled GEMMs by shape (launches, time, TFLOP/s). */
+int wp_runtime_gemm_report(const wp_runtime* rt, char* buf, int capacity);
 
 #ifdef __cplusplus
 }

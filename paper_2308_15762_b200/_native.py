@@ -103,6 +103,7 @@ _SIGS = {
     "wp_runtime_launch_count": (I, [P, I64P]),
     "wp_runtime_set_profiling": (I, [P, I]),
     "wp_runtime_gemm_stats": (I, [P, I64P, DP, DP]),
+    "wp_runtime_gemm_report": (I, [P, C.c_char_p, I]),
 }
 
 EXPORTED = tuple(_SIGS)

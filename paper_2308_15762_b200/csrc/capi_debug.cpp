@@ -8,10 +8,11 @@
 #include "capi_internal.hpp"
 #include "kernels/gemm.cuh"
 
-extern "C" int wp_debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype, const void* a, int64_t lda,
+static int debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype, const void* a, int64_t lda,
                              int a_mn, int64_t a_b1, int64_t a_b2, const void* b, int64_t ldb, int b_mn,
                              int64_t b_b1, int64_t b_b2, int mode, float alpha, void* c, int c_dtype, int64_t ldc,
-                             int64_t c_b1, int64_t c_b2, const float* bias, const void* resid, void* aux) {
+                             int64_t c_b1, int64_t c_b2, const float* bias, const void* resid, void* aux,
+                             int causal) {
   try {
     wpk::GemmProblem g;
     g.M = M;
@@ -20,6 +21,7 @@ extern "C" int wp_debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype
     g.nb1 = nb1;
     g.nb2 = nb2;
     g.in_dtype = in_dtype;
+    g.causal = causal;
     g.A = wpk::Operand{a, lda, a_mn != 0, a_b1, a_b2};
     g.B = wpk::Operand{b, ldb, b_mn != 0, b_b1, b_b2};
     g.epi.mode = mode;
@@ -40,4 +42,21 @@ extern "C" int wp_debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype
   } catch (...) {
     return wpc::map_exception();
   }
+}
+
+extern "C" int wp_debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype, const void* a, int64_t lda,
+                             int a_mn, int64_t a_b1, int64_t a_b2, const void* b, int64_t ldb, int b_mn,
+                             int64_t b_b1, int64_t b_b2, int mode, float alpha, void* c, int c_dtype, int64_t ldc,
+                             int64_t c_b1, int64_t c_b2, const float* bias, const void* resid, void* aux) {
+  return debug_gemm(M, N, K, nb1, nb2, in_dtype, a, lda, a_mn, a_b1, a_b2, b, ldb, b_mn, b_b1, b_b2, mode, alpha, c,
+                    c_dtype, ldc, c_b1, c_b2, bias, resid, aux, 0);
+}
+
+extern "C" int wp_debug_gemm_causal(int M, int N, int K, int nb1, int nb2, int in_dtype, const void* a, int64_t lda,
+                                    int a_mn, int64_t a_b1, int64_t a_b2, const void* b, int64_t ldb, int b_mn,
+                                    int64_t b_b1, int64_t b_b2, int mode, float alpha, void* c, int c_dtype,
+                                    int64_t ldc, int64_t c_b1, int64_t c_b2, const float* bias, const void* resid,
+                                    void* aux, int causal) {
+  return debug_gemm(M, N, K, nb1, nb2, in_dtype, a, lda, a_mn, a_b1, a_b2, b, ldb, b_mn, b_b1, b_b2, mode, alpha, c,
+                    c_dtype, ldc, c_b1, c_b2, bias, resid, aux, causal);
 }

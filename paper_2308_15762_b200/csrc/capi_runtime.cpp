@@ -1,6 +1,7 @@
 // C ABI of the GPU runtime (include/wavepipe.h, "GPU runtime" section).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include <memory>
@@ -150,6 +151,15 @@ int wp_runtime_set_profiling(wp_runtime* rt, int enabled) {
 int wp_runtime_gemm_stats(const wp_runtime* rt, int64_t* launches, double* flops, double* seconds) {
   if (!rt || !launches || !flops || !seconds) return fail(WP_ERR_CONFIG, "null argument");
   rt->rt->gemm_stats(launches, flops, seconds);
+  return WP_OK;
+}
+
+int wp_runtime_gemm_report(const wp_runtime* rt, char* buf, int capacity) {
+  if (!rt || !buf || capacity <= 0) return fail(WP_ERR_CONFIG, "null argument");
+  const std::string r = rt->rt->gemm_report();
+  const size_t n = std::min(r.size(), static_cast<size_t>(capacity - 1));
+  std::memcpy(buf, r.data(), n);
+  buf[n] = 0;
   return WP_OK;
 }
 

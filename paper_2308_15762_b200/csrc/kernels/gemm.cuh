@@ -48,10 +48,22 @@ struct Epilogue {
   void* aux = nullptr;          // same dtype/ld as C (kEpiGelu out, kEpiDGelu in)
 };
 
+// Causal structure inside each batch element (an s x s attention block,
+// queries on M for kCausalSkipUpper / kCausalKUpToRow, keys on M for
+// kCausalKFromRow).  Tiles / K blocks that only touch masked entries are not
+// computed; the consumers never read those outputs.
+enum CausalMode : int {
+  kCausalNone = 0,
+  kCausalSkipUpper = 1,  // C = Q K^T-like: skip output tiles entirely above the diagonal
+  kCausalKUpToRow = 2,   // C = P V-like: K (keys) limited to <= the tile's last row
+  kCausalKFromRow = 3,   // C = P^T dO-like: K (queries) starts at the tile's first row
+};
+
 struct GemmProblem {
   int M = 0, N = 0, K = 0;
   int nb1 = 1, nb2 = 1;
   int in_dtype = kBF16;  // A and B element type
+  int causal = kCausalNone;
   Operand A, B;
   Epilogue epi;
 };

@@ -15,7 +15,7 @@ namespace {
 constexpr int TM = 64, TN = 64, TK = 16;
 
 struct SimtParams {
-  int M, N, K, nb1;
+  int M, N, K, nb1, causal;
   Operand A, B;
   Epilogue epi;
 };
@@ -36,6 +36,11 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtParams p) {
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;
 
+  // Causal K ranges on the 128-wide tiles the softmax writes (gemm.cuh).
+  int k_lo = 0, k_hi = p.K;
+  if (p.causal == kCausalKUpToRow) k_hi = min(p.K, ((m0 + TM - 1) / 128 + 1) * 128);
+  if (p.causal == kCausalKFromRow) k_lo = (m0 / 128) * 128;
+
   // Each thread stages 4 A and 4 B elements per K step.
   auto stage = [&](int buf, int k0) {
 #pragma unroll
@@ -44,21 +49,21 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtParams p) {
       int r, k;
       if (p.A.mn_major) { r = e % TM; k = e / TM; } else { k = e % TK; r = e / TK; }
       const int gm = m0 + r, gk = k0 + k;
-      As[buf][k][r] = (gm < p.M && gk < p.K) ? ld_op(p.A, za, gm, gk) : 0.0f;
+      As[buf][k][r] = (gm < p.M && gk < k_hi) ? ld_op(p.A, za, gm, gk) : 0.0f;
       if (p.B.mn_major) { r = e % TN; k = e / TN; } else { k = e % TK; r = e / TK; }
       const int gn = n0 + r;
       const int gk2 = k0 + k;
-      Bs[buf][k][r] = (gn < p.N && gk2 < p.K) ? ld_op(p.B, zb, gn, gk2) : 0.0f;
+      Bs[buf][k][r] = (gn < p.N && gk2 < k_hi) ? ld_op(p.B, zb, gn, gk2) : 0.0f;
     }
   };
 
   float acc[4][4] = {};
-  const int nk = (p.K + TK - 1) / TK;
-  stage(0, 0);
+  const int nk = (k_hi - k_lo + TK - 1) / TK;
+  stage(0, k_lo);
   __syncthreads();
   for (int kt = 0; kt < nk; ++kt) {
     const int cur = kt & 1;
-    if (kt + 1 < nk) stage(cur ^ 1, (kt + 1) * TK);
+    if (kt + 1 < nk) stage(cur ^ 1, k_lo + (kt + 1) * TK);
 #pragma unroll
     for (int k = 0; k < TK; ++k) {
       float a[4], b[4];
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtParams p) {
 int gemm_simt(const GemmProblem& g, cudaStream_t s) {
   if (g.in_dtype != kF32) throw std::runtime_error("gemm_simt: inputs must be fp32");
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return 0;
-  SimtParams p{g.M, g.N, g.K, g.nb1, g.A, g.B, g.epi};
+  SimtParams p{g.M, g.N, g.K, g.nb1, g.causal, g.A, g.B, g.epi};
   dim3 grid((g.N + TN - 1) / TN, (g.M + TM - 1) / TM, g.nb1 * g.nb2);
   gemm_simt_kernel<<<grid, 256, 0, s>>>(p);
   return 1;

@@ -1,0 +1,212 @@
+// bf16 GEMM on a CTA pair (tcgen05.mma.cta_group::2): one 256 x 256 output
+// tile per SM pair of a 2-CTA cluster.  Each CTA stages its own 128 rows of A
+// and its own 128 columns of B (TMA .cta_group::2, bytes counted on the
+// leader's barrier); the leader's single MMA thread issues M=256, N=256,
+// K=16 instructions that read both CTAs' shared memory and accumulate rows
+// 0-127 into the leader's TMEM and rows 128-255 into the peer's.  Per SM and
+// K block that is 32 KB of operand traffic for 128x256x64 MACs -- two thirds
+// of the 1-CTA 128 x 256 tile's 48 KB -- which is what lets the tensor pipe
+// stay fed from L2.
+//
+//   warp 0      TMA producer (both CTAs): 6-stage ring of 32 KB stages
+//   warp 1      MMA issuer (leader only): commits multicast to both CTAs
+//   warp 2      TMEM owner (cta_group::2 alloc/dealloc in both CTAs)
+//   warps 4-7   epilogue (both CTAs): own TMEM rows -> fused op -> global;
+//               release the accumulator on the leader's barrier (8 arrivals)
+#include <cstdio>
+#include <stdexcept>
+
+#include "kernels/tc_common.cuh"
+
+namespace wpk {
+namespace tc {
+namespace {
+
+constexpr int PBN = 256;           // pair tile N
+constexpr int HALF_N = PBN / 2;    // columns staged per CTA
+constexpr int PM = 2 * BM;         // pair tile M
+constexpr int P_STAGE_BYTES = A_BYTES + HALF_N * BK * 2;  // 32 KB
+constexpr int P_STAGES = 6;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + P_STAGES;
+  uint64_t* tfull_bar = empty_bar + P_STAGES;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < p.num_tiles; t += npairs) {
+        int mb, nb, z1, z2;
+        decode_tile(p, t, mb, nb, z1, z2);
+        const int row0 = mb * PM + static_cast<int>(rank) * BM;
+        const int col0 = nb * PBN + static_cast<int>(rank) * HALF_N;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * P_STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          if (leader) mbar_expect_tx(&full_bar[stage], 2 * P_STAGE_BYTES);
+          if (!A_MN) {
+            tma_load_4d_pair(&map_a, &full_bar[stage], sa, kb * BK, row0, z1, z2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_4d_pair(&map_a, &full_bar[stage], sa + j * CHUNK_BYTES, row0 + j * 64, kb * BK, z1, z2);
+          }
+          if (!B_MN) {
+            tma_load_4d_pair(&map_b, &full_bar[stage], sb, kb * BK, col0, z1, z2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < HALF_N / 64; ++j)
+              tma_load_4d_pair(&map_b, &full_bar[stage], sb + j * CHUNK_BYTES, col0 + j * 64, kb * BK, z1, z2);
+          }
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(A_MN) << 15) |
+                                 (uint32_t(B_MN) << 16) | (uint32_t(PBN >> 3) << 17) | (uint32_t(PM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * PBN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * P_STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_desc(sa + k * 2048, CHUNK_BYTES, 1024) : make_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(sb + k * 2048, CHUNK_BYTES, 1024) : make_desc(sb + k * 32, 16, 1024);
+            tc_mma_pair(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit_pair(&empty_bar[stage]);  // frees this stage in both CTAs
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(&tfull_bar[acc]);  // both halves of the accumulator ready
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp & 3;
+    int local = 0;
+    for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
+      int mb, nb, z1, z2;
+      decode_tile(p, t, mb, nb, z1, z2);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * PM + static_cast<int>(rank) * BM + ew * 32 + lane;
+      const int64_t zoff = static_cast<int64_t>(z1) * p.epi.c_b1 + static_cast<int64_t>(z2) * p.epi.c_b2;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * PBN;
+      const int col_end = min(PBN, p.N - nb * PBN);
+      for (int c = 0; c < col_end; c += 32) {
+        float v[32];
+        tmem_ld32(taddr + c, v);
+        if (row < p.M) epilogue_chunk(p, v, row, nb * PBN + c, zoff);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 0);
+    }
+  }
+
+  tc_fence_before();
+  __syncwarp();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+template <bool A_MN, bool B_MN>
+void launch_pair(const GemmProblem& g, const Params& p, cudaStream_t s) {
+  auto* k = gemm_tc2_kernel<A_MN, B_MN>;
+  static uint64_t attr_done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_done >> (dev & 63) & 1)) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+    attr_done |= 1ull << (dev & 63);
+  }
+  const CUtensorMap ma = A_MN ? make_map(g.A, g.M, g.K, g.nb1, g.nb2, 64) : make_map(g.A, g.K, g.M, g.nb1, g.nb2, BM);
+  const CUtensorMap mb =
+      B_MN ? make_map(g.B, g.N, g.K, g.nb1, g.nb2, 64) : make_map(g.B, g.K, g.N, g.nb1, g.nb2, HALF_N);
+  const int pairs = std::min(p.num_tiles, num_sms() / 2);
+  k<<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, s>>>(ma, mb, p);
+}
+
+}  // namespace
+
+int gemm_tc2(const GemmProblem& g, cudaStream_t s) {
+  Params p;
+  fill_params(g, p, PM, PBN);
+  const int sel = (g.A.mn_major ? 2 : 0) + (g.B.mn_major ? 1 : 0);
+  switch (sel) {
+    case 0: launch_pair<false, false>(g, p, s); break;
+    case 1: launch_pair<false, true>(g, p, s); break;
+    case 2: launch_pair<true, false>(g, p, s); break;
+    default: launch_pair<true, true>(g, p, s); break;
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc2 launch: ") + cudaGetErrorString(e));
+  return 1;
+}
+
+}  // namespace tc
+}  // namespace wpk

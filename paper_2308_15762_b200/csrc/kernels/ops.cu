@@ -211,11 +211,16 @@ __global__ void __launch_bounds__(256) ln_bwd_dwdb_k(const T* dy, const T* x, co
 
 // ------------------------------------------------------------------- softmax
 // Warp per row; lane l holds columns l + 32*k.
+// Causal rows only touch columns j <= q; P is written up to the end of q's
+// 128-wide tile (zeros past the diagonal) -- exactly the K range the causal
+// P.V / dS.K GEMMs read (kCausalKUpToRow) -- and not beyond.
 template <typename T>
 __global__ void __launch_bounds__(256) softmax_fwd_k(const float* S, T* P, int rows, int n, int causal) {
   const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (row >= rows) return;
   const int q = row % n;
+  const int valid = causal ? q + 1 : n;
+  const int lim = causal ? min(n, (q / 128 + 1) * 128) : n;
   const float* sr = S + static_cast<int64_t>(row) * n;
   T* pr = P + static_cast<int64_t>(row) * n;
   float v[32];
@@ -223,7 +228,7 @@ __global__ void __launch_bounds__(256) softmax_fwd_k(const float* S, T* P, int r
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
     const int j = lane + 32 * k;
-    v[k] = (j < n && !(causal && j > q)) ? sr[j] : -INFINITY;
+    v[k] = j < valid ? sr[j] : -INFINITY;
     m = fmaxf(m, v[k]);
   }
   m = warp_max(m);
@@ -237,14 +242,18 @@ __global__ void __launch_bounds__(256) softmax_fwd_k(const float* S, T* P, int r
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
     const int j = lane + 32 * k;
-    if (j < n) pr[j] = from_f<T>(v[k] * inv);
+    if (j < lim) pr[j] = from_f<T>(v[k] * inv);
   }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) softmax_bwd_k(const float* dP, T* P, int rows, int n, float scale) {
+__global__ void __launch_bounds__(256) softmax_bwd_k(const float* dP, T* P, int rows, int n, float scale,
+                                                     int causal) {
   const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (row >= rows) return;
+  const int q = row % n;
+  const int valid = causal ? q + 1 : n;
+  const int lim = causal ? min(n, (q / 128 + 1) * 128) : n;
   const float* dr = dP + static_cast<int64_t>(row) * n;
   T* pr = P + static_cast<int64_t>(row) * n;
   float p[32], d[32];
@@ -252,15 +261,15 @@ __global__ void __launch_bounds__(256) softmax_bwd_k(const float* dP, T* P, int 
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
     const int j = lane + 32 * k;
-    p[k] = j < n ? to_f(pr[j]) : 0.f;
-    d[k] = j < n ? dr[j] : 0.f;
+    p[k] = j < valid ? to_f(pr[j]) : 0.f;
+    d[k] = j < valid ? dr[j] : 0.f;
     dot += p[k] * d[k];
   }
   dot = warp_sum(dot);
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
     const int j = lane + 32 * k;
-    if (j < n) pr[j] = from_f<T>(scale * p[k] * (d[k] - dot));
+    if (j < lim) pr[j] = from_f<T>(scale * p[k] * (d[k] - dot));
   }
 }
 
@@ -322,14 +331,34 @@ __global__ void __launch_bounds__(256) xent_k(T* logits, const int32_t* labels, 
 }
 
 // --------------------------------------------------------------- bias grads
+// Block = 8 warps over a 256-column strip; lane owns 8 contiguous columns
+// (one 16-byte load per row for bf16), warps stride over the block's rows,
+// partials reduced through shared memory, one atomic per column per block.
 template <typename T>
-__global__ void colsum_k(const T* dy, float* db, int T_, int n, int ld, int rows_per) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= n) return;
+__global__ void __launch_bounds__(256) colsum_k(const T* dy, float* db, int T_, int n, int ld, int rows_per) {
+  __shared__ float red[8][256];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int col = blockIdx.x * 256 + lane * 8;
   const int r0 = blockIdx.y * rows_per, r1 = min(T_, r0 + rows_per);
-  float s = 0.f;
-  for (int r = r0; r < r1; ++r) s += to_f(dy[static_cast<int64_t>(r) * ld + col]);
-  atomicAdd(&db[col], s);
+  float acc[8] = {};
+  if (col < n) {
+    for (int r = r0 + warp; r < r1; r += 8) {
+      float v[8];
+      load8(dy + static_cast<int64_t>(r) * ld + col, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += v[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) red[warp][lane * 8 + k] = acc[k];
+  __syncthreads();
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+    atomicAdd(&db[c], t);
+  }
 }
 
 // ---------------------------------------------------------------- optimizer
@@ -480,11 +509,11 @@ int softmax_fwd(int dtype, const float* S, void* P, int rows, int n, int causal,
   return 1;
 }
 
-int softmax_bwd(int dtype, const float* dP, void* P, int rows, int n, float scale, cudaStream_t s) {
+int softmax_bwd(int dtype, const float* dP, void* P, int rows, int n, float scale, int causal, cudaStream_t s) {
   if (n > 1024) throw std::runtime_error("softmax: row length must be <= 1024");
   const int grid = (rows + 7) / 8;
-  if (dtype == kBF16) softmax_bwd_k<bf16><<<grid, 256, 0, s>>>(dP, static_cast<bf16*>(P), rows, n, scale);
-  else softmax_bwd_k<float><<<grid, 256, 0, s>>>(dP, static_cast<float*>(P), rows, n, scale);
+  if (dtype == kBF16) softmax_bwd_k<bf16><<<grid, 256, 0, s>>>(dP, static_cast<bf16*>(P), rows, n, scale, causal);
+  else softmax_bwd_k<float><<<grid, 256, 0, s>>>(dP, static_cast<float*>(P), rows, n, scale, causal);
   check_launch("softmax_bwd");
   return 1;
 }
@@ -500,10 +529,11 @@ int xent_fwd_bwd(int dtype, void* logits, const int32_t* labels, float* loss, in
 }
 
 int colsum_accum(int dtype, const void* dy, float* db, int T_, int n, int ld, cudaStream_t s) {
+  if (n % 8 || ld % 8) throw std::runtime_error("colsum: columns and leading dimension must be multiples of 8");
   const int rows_per = 128;
-  const dim3 grid((n + 127) / 128, (T_ + rows_per - 1) / rows_per);
-  if (dtype == kBF16) colsum_k<bf16><<<grid, 128, 0, s>>>(static_cast<const bf16*>(dy), db, T_, n, ld, rows_per);
-  else colsum_k<float><<<grid, 128, 0, s>>>(static_cast<const float*>(dy), db, T_, n, ld, rows_per);
+  const dim3 grid((n + 255) / 256, (T_ + rows_per - 1) / rows_per);
+  if (dtype == kBF16) colsum_k<bf16><<<grid, 256, 0, s>>>(static_cast<const bf16*>(dy), db, T_, n, ld, rows_per);
+  else colsum_k<float><<<grid, 256, 0, s>>>(static_cast<const float*>(dy), db, T_, n, ld, rows_per);
   check_launch("colsum");
   return 1;
 }

@@ -25,10 +25,12 @@ int layernorm_bwd(int dtype, const void* dy, const void* x, const float* mean, c
                   const void* dres, void* dx, float* dw, float* db, int T, int h, cudaStream_t s);
 
 // Row softmax of fp32 scores S [rows, n] -> P (act dtype); causal masks
-// column j > (row % n) (query position).  Scale already applied to S.
+// column j > (row % n) (query position) and reads/writes only up to the end
+// of the query's 128-wide tile.  Scale already applied to S.
 int softmax_fwd(int dtype, const float* S, void* P, int rows, int n, int causal, cudaStream_t s);
 // dS = scale * P * (dP - sum(dP*P)), written over P (act dtype).
-int softmax_bwd(int dtype, const float* dP, void* P_inout, int rows, int n, float scale, cudaStream_t s);
+int softmax_bwd(int dtype, const float* dP, void* P_inout, int rows, int n, float scale, int causal,
+                cudaStream_t s);
 
 // Fused cross-entropy: per row, loss += (lse - logit[label]) * loss_scale into
 // *loss_accum (fp32 device scalar); logits overwritten with

@@ -1,0 +1,304 @@
+// Shared pieces of the tcgen05 GEMM kernels (1-CTA gemm_tc.cu, CTA-pair
+// gemm_tc2.cu): PTX wrappers for mbarrier / TMA / tcgen05, the SW128 smem
+// descriptor, tile decoding and the fused epilogue.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "kernels/gemm.cuh"
+
+namespace wpk {
+namespace tc {
+
+constexpr int BM = 128, BK = 64;
+constexpr int A_BYTES = BM * BK * 2;      // 16 KB
+constexpr int CHUNK_BYTES = 64 * BK * 2;  // one 64(MN) x 64(K) SW128 box, 8 KB
+constexpr int NUM_THREADS = 256;
+constexpr int TMEM_COLS = 512;
+
+// Tile width N: 256 for the linear layers, 128 when N <= 128 (attention's
+// head dimension) so no MMA column is spent on zero padding.
+template <int BN>
+struct TileCfg {
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+struct Params {
+  int M, N, K, nb1, nb2;
+  int tiles_m, tiles_n, num_tiles, k_blocks;
+  int vec_ok;
+  int causal;  // kCausal* (gemm.cuh): per-tile skip / K range inside each s x s block
+  Epilogue epi;
+};
+
+// K-block range [kb0, kb1) of output tile (m_blk, n_blk); empty = skip tile.
+template <int BN>
+__device__ __forceinline__ void k_range(const Params& p, int m_blk, int n_blk, int& kb0, int& kb1) {
+  kb0 = 0;
+  kb1 = p.k_blocks;
+  if (p.causal == kCausalSkipUpper) {
+    if (n_blk * BN > m_blk * BM + BM - 1) kb1 = 0;  // every key after every query
+  } else if (p.causal == kCausalKUpToRow) {
+    kb1 = min(kb1, (m_blk * BM + BM + BK - 1) / BK);
+  } else if (p.causal == kCausalKFromRow) {
+    kb0 = (m_blk * BM) / BK;
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// 32 lanes x 32 consecutive fp32 columns: thread i gets row (lane base + i).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bits.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(lbo_bytes >> 4) << 16) |
+         (static_cast<uint64_t>(sbo_bytes >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ void decode_tile(const Params& p, int t, int& m_blk, int& n_blk, int& z1, int& z2) {
+  m_blk = t % p.tiles_m;
+  int r = t / p.tiles_m;
+  n_blk = r % p.tiles_n;
+  const int z = r / p.tiles_n;
+  z1 = z % p.nb1;
+  z2 = z / p.nb1;
+}
+
+__device__ __forceinline__ float load_elem(const void* base, int dtype, int64_t off) {
+  return dtype == kF32 ? static_cast<const float*>(base)[off]
+                       : __bfloat162float(static_cast<const __nv_bfloat16*>(base)[off]);
+}
+
+__device__ __forceinline__ void store_elem(void* base, int dtype, int64_t off, float v) {
+  if (dtype == kF32) static_cast<float*>(base)[off] = v;
+  else static_cast<__nv_bfloat16*>(base)[off] = __float2bfloat16_rn(v);
+}
+
+// Epilogue for one row segment of 32 columns starting at (row, col0).
+__device__ __forceinline__ void epilogue_chunk(const Params& p, const float* acc, int row, int col0,
+                                               int64_t zoff) {
+  const Epilogue& e = p.epi;
+  const int64_t base = zoff + static_cast<int64_t>(row) * e.ldc + col0;
+  const int ncols = min(32, p.N - col0);
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = acc[i] * e.alpha;
+  if (e.bias) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < ncols) v[i] += e.bias[col0 + i];
+  }
+  const bool vec = p.vec_ok && ncols == 32;
+  if (e.mode == kEpiAccum) {  // fp32 C
+    float* c = static_cast<float*>(e.c) + base;
+    if (vec) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        float4 o = *reinterpret_cast<float4*>(c + i);
+        o.x += v[i];
+        o.y += v[i + 1];
+        o.z += v[i + 2];
+        o.w += v[i + 3];
+        *reinterpret_cast<float4*>(c + i) = o;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < ncols) c[i] += v[i];
+    }
+    return;
+  }
+  if (e.mode == kEpiResidual) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < ncols) v[i] += load_elem(e.resid, e.c_dtype, base + i);
+  } else if (e.mode == kEpiGelu) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (i < ncols) {
+        // GELU of the pre-activation as stored, so backward sees the same value.
+        const float pre = e.c_dtype == kF32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
+        store_elem(e.aux, e.c_dtype, base + i, pre);
+        v[i] = gelu_f(pre);
+      }
+    }
+  } else if (e.mode == kEpiDGelu) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < ncols) v[i] *= gelu_grad_f(load_elem(e.aux, e.c_dtype, base + i));
+  }
+  if (e.c_dtype == kBF16) {
+    __nv_bfloat16* c = static_cast<__nv_bfloat16*>(e.c) + base;
+    if (vec) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 pk;
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[i], v[i + 1]);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
+        pk.x = *reinterpret_cast<uint32_t*>(&h0);
+        pk.y = *reinterpret_cast<uint32_t*>(&h1);
+        pk.z = *reinterpret_cast<uint32_t*>(&h2);
+        pk.w = *reinterpret_cast<uint32_t*>(&h3);
+        *reinterpret_cast<uint4*>(c + i) = pk;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < ncols) c[i] = __float2bfloat16_rn(v[i]);
+    }
+  } else {
+    float* c = static_cast<float*>(e.c) + base;
+    if (vec) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < ncols) c[i] = v[i];
+    }
+  }
+}
+
+
+// --- CTA-pair (cta_group::2) variants -------------------------------------
+// TMA load whose completion is counted on the pair leader's mbarrier (the
+// peer bit of the shared::cluster barrier address cleared).
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
+
+__device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                                 int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar) & kPeerBitMask)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Arrive on the barrier at the same offset in both CTAs of the pair.
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b16 m;\n"
+      "mov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Arrive on the barrier at `bar`'s offset in cluster CTA `rank`.
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encoder();
+CUtensorMap make_map(const Operand& op, int64_t inner, int64_t outer, int nb1, int nb2, int box_outer);
+int num_sms();
+void fill_params(const GemmProblem& g, Params& p, int tile_m, int tile_n);
+int gemm_tc2(const GemmProblem& g, cudaStream_t s);  // CTA-pair kernel, 256 x 256 tiles
+
+}  // namespace tc
+}  // namespace wpk

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -126,6 +127,10 @@ struct DeviceState {
   std::vector<cudaEvent_t> events;
   size_t ev_next = 0;
   std::vector<uint8_t> published_at;  // BE positions whose outgoing message is published
+  // NCCL transport: per-peer send / receive streams and the step's posted
+  // receives (landing buffer + arrival event per message).
+  std::map<int, cudaStream_t> tx, rx;
+  std::map<MsgKey, std::pair<BufPtr, cudaEvent_t>> posted;
 
   struct Rec {
     int idx;
@@ -144,6 +149,7 @@ struct DeviceState {
   struct GemmRec {
     double flops;
     cudaEvent_t s, e;
+    std::string shape;
   };
   std::vector<GemmRec> gemm_recs;
 };
@@ -177,10 +183,68 @@ Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, in
     ncclComm_t comm;
     ckn(NcclApi::get().CommInitRank(&comm, P, id, rank_), "ncclCommInitRank");
     nccl_comm_ = comm;
+    build_channels();
+  }
+}
+
+void Runtime::build_channels() {
+  // Sender-order message lists per directed pair, from the full list every
+  // rank holds; then one ncclCommSplit per pair, called by every rank in the
+  // same order (collective), members keyed sender=0 / receiver=1.
+  std::map<std::pair<int, int>, std::vector<MsgKey>> plan;
+  for (int p = 0; p < list_.config.devices; ++p)
+    for (const Action& a : list_.per_device[p])
+      if (a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange) plan[{p, a.peer}].push_back(key_of(a));
+  DeviceState& d = *devs_[0];
+  DevGuard g(d.cuda);
+  for (auto& [pair, keys] : plan) {
+    Channel c;
+    c.src = pair.first;
+    c.dst = pair.second;
+    c.keys = keys;
+    const bool member = rank_ == c.src || rank_ == c.dst;
+    ncclComm_t sub = nullptr;
+    ckn(NcclApi::get().CommSplit(static_cast<ncclComm_t>(nccl_comm_), member ? static_cast<int>(channels_.size()) : -1,
+                                 rank_ == c.src ? 0 : 1, &sub, nullptr),
+        "ncclCommSplit");
+    c.comm = sub;
+    if (rank_ == c.src && !d.tx.count(c.dst)) {
+      cudaStream_t s;
+      ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+      d.tx[c.dst] = s;
+    }
+    if (rank_ == c.dst && !d.rx.count(c.src)) {
+      cudaStream_t s;
+      ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+      d.rx[c.src] = s;
+    }
+    channels_.push_back(c);
+  }
+}
+
+void Runtime::post_channel_receives(DeviceState& d) {
+  // Every incoming message of the step, per channel in the sender's order:
+  // NCCL matches a pair's messages FIFO, so posting in sender order gives
+  // each message its own landing buffer whatever order this device consumes
+  // them in.  Receives wait on nothing but earlier receives of the channel.
+  const size_t bytes = size_t(m_.tokens()) * m_.hidden * m_.act_bytes();
+  for (const Channel& c : channels_) {
+    if (c.dst != d.pipe) continue;
+    cudaStream_t s = d.rx.at(c.src);
+    ck(cudaStreamWaitEvent(s, d.step_begin, 0), "rx after begin");
+    for (const MsgKey& k : c.keys) {
+      BufPtr landing = d.pool->alloc(bytes, s, 1);
+      ckn(NcclApi::get().Recv(landing->p, bytes, ncclUint8, 0, static_cast<ncclComm_t>(c.comm), s), "ncclRecv");
+      cudaEvent_t arrive = next_event(d);
+      ck(cudaEventRecord(arrive, s), "record arrival");
+      d.posted[k] = {landing, arrive};
+    }
   }
 }
 
 Runtime::~Runtime() {
+  for (auto& c : channels_)
+    if (c.comm) NcclApi::get().CommDestroy(static_cast<ncclComm_t>(c.comm));
   if (nccl_comm_) NcclApi::get().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
   for (auto& d : devs_) {
     DevGuard g(d->cuda);
@@ -194,6 +258,8 @@ Runtime::~Runtime() {
     d->pool.reset();
     if (d->compute) cudaStreamDestroy(d->compute);
     if (d->copy) cudaStreamDestroy(d->copy);
+    for (auto& kv : d->tx) cudaStreamDestroy(kv.second);
+    for (auto& kv : d->rx) cudaStreamDestroy(kv.second);
   }
 }
 
@@ -323,7 +389,10 @@ void Runtime::gemm(DeviceState& d, const wpk::GemmProblem& g) {
   ck(cudaEventRecord(s, d.compute), "record gemm start");
   launches_ += wpk::gemm(g, d.compute);
   ck(cudaEventRecord(e, d.compute), "record gemm end");
-  d.gemm_recs.push_back({2.0 * g.M * g.N * g.K * g.nb1 * g.nb2, s, e});
+  const std::string shape = std::to_string(g.M) + "x" + std::to_string(g.N) + "x" + std::to_string(g.K) + " b" +
+                            std::to_string(g.nb1 * g.nb2) + " " + (g.A.mn_major ? "M" : "K") +
+                            (g.B.mn_major ? "N" : "K") + " c" + std::to_string(g.causal);
+  d.gemm_recs.push_back({2.0 * g.M * g.N * g.K * g.nb1 * g.nb2, s, e, shape});
 }
 
 cudaEvent_t Runtime::next_event(DeviceState& d) {
@@ -384,6 +453,7 @@ BufPtr Runtime::unit_fwd(DeviceState& d, int ui, int mb, BufPtr x, UnitStash& st
     wpk::GemmProblem sg;
     sg.in_dtype = dt;
     sg.M = S, sg.N = S, sg.K = dh, sg.nb1 = H, sg.nb2 = m_.mbs;
+    sg.causal = m_.causal ? wpk::kCausalSkipUpper : wpk::kCausalNone;
     sg.A = op(st.a->p, 3 * h, false, dh, int64_t(S) * 3 * h);
     sg.B = op(at(st.a, h, es), 3 * h, false, dh, int64_t(S) * 3 * h);
     sg.epi.c = d.scores, sg.epi.c_dtype = wpk::kF32, sg.epi.ldc = S, sg.epi.c_b1 = int64_t(S) * S,
@@ -396,6 +466,7 @@ BufPtr Runtime::unit_fwd(DeviceState& d, int ui, int mb, BufPtr x, UnitStash& st
     wpk::GemmProblem pv;
     pv.in_dtype = dt;
     pv.M = S, pv.N = dh, pv.K = S, pv.nb1 = H, pv.nb2 = m_.mbs;
+    pv.causal = m_.causal ? wpk::kCausalKUpToRow : wpk::kCausalNone;
     pv.A = op(st.b->p, S, false, int64_t(S) * S, int64_t(H) * S * S);
     pv.B = op(at(st.a, 2 * h, es), 3 * h, true, dh, int64_t(S) * 3 * h);
     pv.epi.c = st.c->p, pv.epi.c_dtype = dt, pv.epi.ldc = h, pv.epi.c_b1 = dh, pv.epi.c_b2 = int64_t(S) * h;
@@ -528,6 +599,7 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     wpk::GemmProblem g;
     g.in_dtype = dt;
     g.M = S, g.N = S, g.K = dh, g.nb1 = H, g.nb2 = m_.mbs;
+    g.causal = m_.causal ? wpk::kCausalSkipUpper : wpk::kCausalNone;
     g.A = op(dctx->p, h, false, dh, int64_t(S) * h);
     g.B = op(at(st.a, 2 * h, es), 3 * h, false, dh, int64_t(S) * 3 * h);
     g.epi.c = d.scores, g.epi.c_dtype = wpk::kF32, g.epi.ldc = S, g.epi.c_b1 = int64_t(S) * S,
@@ -540,6 +612,7 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     wpk::GemmProblem g;
     g.in_dtype = dt;
     g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
+    g.causal = m_.causal ? wpk::kCausalKFromRow : wpk::kCausalNone;
     g.A = op(st.b->p, S, true, int64_t(S) * S, int64_t(H) * S * S);
     g.B = op(dctx->p, h, true, dh, int64_t(S) * h);
     g.epi.c = at(dqkv, 2 * h, es), g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh,
@@ -548,12 +621,13 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   }
   // dS = P * (dP - rowsum(dP * P)) / sqrt(d), in place over P
   launches_ += wpk::softmax_bwd(dt, d.scores, st.b->p, m_.mbs * H * S, S, 1.0f / std::sqrt(static_cast<float>(dh)),
-                                cs);
+                                m_.causal, cs);
   // dQ = dS K
   {
     wpk::GemmProblem g;
     g.in_dtype = dt;
     g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
+    g.causal = m_.causal ? wpk::kCausalKUpToRow : wpk::kCausalNone;
     g.A = op(st.b->p, S, false, int64_t(S) * S, int64_t(H) * S * S);
     g.B = op(at(st.a, h, es), 3 * h, true, dh, int64_t(S) * 3 * h);
     g.epi.c = dqkv->p, g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh, g.epi.c_b2 = int64_t(S) * 3 * h;
@@ -564,6 +638,7 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     wpk::GemmProblem g;
     g.in_dtype = dt;
     g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
+    g.causal = m_.causal ? wpk::kCausalKFromRow : wpk::kCausalNone;
     g.A = op(st.b->p, S, true, int64_t(S) * S, int64_t(H) * S * S);
     g.B = op(st.a->p, 3 * h, true, dh, int64_t(S) * 3 * h);
     g.epi.c = at(dqkv, h, es), g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh,
@@ -660,7 +735,6 @@ bool Runtime::advance(DeviceState& d) {
   const auto& prog = list_.per_device[d.pipe];
   bool moved = false;
   DevGuard g(d.cuda);
-  ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm_);
   while (d.pc < prog.size()) {
     const Action& a = prog[d.pc];
     if (a.is_compute()) {
@@ -678,35 +752,38 @@ bool Runtime::advance(DeviceState& d) {
     } else if (a.kind == ActionKind::OptimizerStep) {
       optimizer(d);
     } else if (transport_ == WP_TRANSPORT_NCCL) {
-      // One in-order NCCL stream per rank; BE = grouped send+recv (rendezvous-safe).
-      const MsgKey out = key_of(a);
-      auto recv_into = [&](const MsgKey& kin, int peer, size_t bytes) {
-        BufPtr landing = d.pool->alloc(bytes, d.copy, 1);
-        ckn(NcclApi::get().Recv(landing->p, bytes, ncclUint8, peer, comm, d.copy), "ncclRecv");
-        d.inbox[kin] = landing;
+      // Receives were posted at step start (post_channel_receives); here a
+      // Receive / the incoming half of an exchange only gates the next
+      // compute on that message's arrival.  Sends go out on the per-peer tx
+      // stream right after their producer -- buffered, never blocking compute.
+      auto arrive = [&](const MsgKey& kin) {
+        auto it = d.posted.find(kin);
+        if (it == d.posted.end()) throw wavepipe::SimulationError("runtime: message was not posted");
+        d.inbox[kin] = it->second.first;
+        d.pending.push_back(it->second.second);
+        d.posted.erase(it);
       };
-      const size_t msg_bytes = size_t(m_.tokens()) * m_.hidden * m_.act_bytes();
       if (a.kind == ActionKind::Receive) {
-        ck(cudaStreamWaitEvent(d.copy, d.last_start ? d.last_start : d.step_begin, 0), "wait post");
-        recv_into(key_of(a), a.peer, msg_bytes);
+        arrive(key_of(a));
       } else {
+        const MsgKey out = key_of(a);
         auto it = d.outbox.find(out);
         if (it == d.outbox.end()) throw wavepipe::SimulationError("runtime: send before its producer");
-        ck(cudaStreamWaitEvent(d.copy, d.outbox_ready[out], 0), "wait ready");
-        if (a.kind == ActionKind::BatchedExchange) ckn(NcclApi::get().GroupStart(), "group");
-        ckn(NcclApi::get().Send(it->second->p, msg_bytes, ncclUint8, a.peer, comm, d.copy), "ncclSend");
+        const Channel* ch = nullptr;
+        for (const Channel& c : channels_)
+          if (c.src == d.pipe && c.dst == a.peer) ch = &c;
+        cudaStream_t s = d.tx.at(a.peer);
+        ck(cudaStreamWaitEvent(s, d.outbox_ready[out], 0), "wait ready");
+        const size_t msg_bytes = size_t(m_.tokens()) * m_.hidden * m_.act_bytes();
+        ckn(NcclApi::get().Send(it->second->p, msg_bytes, ncclUint8, 1, static_cast<ncclComm_t>(ch->comm), s),
+            "ncclSend");
+        d.pool->release(it->second, s);
+        d.outbox.erase(it);
+        d.outbox_ready.erase(out);
         if (a.kind == ActionKind::BatchedExchange) {
           const auto [q, qi] = d.be_partner[d.pc];
-          recv_into(key_of(list_.per_device[q][qi]), a.peer, msg_bytes);
-          ckn(NcclApi::get().GroupEnd(), "group");
+          arrive(key_of(list_.per_device[q][qi]));
         }
-        d.pool->release(it->second, d.copy);
-        d.outbox.erase(it);
-      }
-      if (a.kind != ActionKind::Send) {  // only incoming data gates the next compute
-        cudaEvent_t arrive = next_event(d);
-        ck(cudaEventRecord(arrive, d.copy), "record arrival");
-        d.pending.push_back(arrive);
       }
     } else {
       // In-process transport.
@@ -784,17 +861,21 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     d->published_at.assign(list_.per_device[d->pipe].size(), 0);
     ck(cudaEventRecord(d->step_begin, d->compute), "record step begin");
     ck(cudaStreamWaitEvent(d->copy, d->step_begin, 0), "copy after begin");
+    if (transport_ == WP_TRANSPORT_NCCL) post_channel_receives(*d);
   }
   enqueue_step();
   float loss = 0.f;
   for (auto& d : devs_) {
     DevGuard g(d->cuda);
     ck(cudaStreamSynchronize(d->copy), "step sync");
+    for (auto& kv : d->tx) ck(cudaStreamSynchronize(kv.second), "step sync");
+    for (auto& kv : d->rx) ck(cudaStreamSynchronize(kv.second), "step sync");
     ck(cudaStreamSynchronize(d->compute), "step sync");
     float l = 0.f;
     ck(cudaMemcpy(&l, d->loss, sizeof(float), cudaMemcpyDeviceToHost), "loss D2H");
     loss += l;
-    if (!d->stash.empty() || !d->handoff.empty() || !d->inbox.empty() || !d->outbox.empty()) {
+    if (!d->stash.empty() || !d->handoff.empty() || !d->inbox.empty() || !d->outbox.empty() ||
+        !d->posted.empty()) {
       throw wavepipe::SimulationError("runtime: state left over at the end of the step");
     }
   }
@@ -807,6 +888,10 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
       prof_seconds_ += 1e-3 * ms;
       prof_flops_ += r.flops;
       ++prof_launches_;
+      auto& st = prof_shapes_[r.shape];
+      ++st.n;
+      st.flops += r.flops;
+      st.seconds += 1e-3 * ms;
     }
   }
   ++step_;
@@ -846,6 +931,20 @@ void Runtime::collect_trace() {
               return std::tie(x.arrival_time, x.post_time, x.src_device, x.dst_device) <
                      std::tie(y.arrival_time, y.post_time, y.src_device, y.dst_device);
             });
+}
+
+std::string Runtime::gemm_report() const {
+  std::vector<std::pair<double, std::string>> rows;
+  for (const auto& [k, v] : prof_shapes_) {
+    char line[256];
+    std::snprintf(line, sizeof line, "%-36s n=%6lld  %9.3f ms  %7.1f TFLOP/s\n", k.c_str(),
+                  static_cast<long long>(v.n), 1e3 * v.seconds, v.seconds > 0 ? v.flops / v.seconds / 1e12 : 0.0);
+    rows.emplace_back(v.seconds, line);
+  }
+  std::sort(rows.rbegin(), rows.rend());
+  std::string out;
+  for (auto& r : rows) out += r.second;
+  return out;
 }
 
 // ------------------------------------------------------------- parameters

@@ -111,7 +111,12 @@ class Runtime {
     *flops = prof_flops_;
     *seconds = prof_seconds_;
   }
-  void reset_gemm_stats() { prof_launches_ = 0, prof_flops_ = 0, prof_seconds_ = 0; }
+  void reset_gemm_stats() {
+    prof_launches_ = 0, prof_flops_ = 0, prof_seconds_ = 0;
+    prof_shapes_.clear();
+  }
+  // Per GEMM shape: "MxNxK b<batch> <A,B majorness> c<causal>" -> (launches, flops, seconds).
+  std::string gemm_report() const;
   int64_t launches() const { return launches_; }
 
   int param_count() const { return static_cast<int>(param_index_.size()); }
@@ -162,10 +167,25 @@ class Runtime {
   bool tracing_ = false, update_ = true, profiling_ = false;
   int64_t prof_launches_ = 0;
   double prof_flops_ = 0, prof_seconds_ = 0;
+  struct ShapeStat {
+    int64_t n = 0;
+    double flops = 0, seconds = 0;
+  };
+  std::map<std::string, ShapeStat> prof_shapes_;
   int step_ = 0;
   int64_t launches_ = 0;
   wavepipe::SimTrace trace_;
-  void* nccl_comm_ = nullptr;
+  void* nccl_comm_ = nullptr;  // world communicator (NCCL transport)
+  // One communicator per directed device pair (sender rank 0, receiver rank
+  // 1 inside it) and the pair's messages in the sender's program order.
+  struct Channel {
+    int src, dst;
+    void* comm = nullptr;
+    std::vector<MsgKey> keys;
+  };
+  std::vector<Channel> channels_;
+  void build_channels();
+  void post_channel_receives(DeviceState& d);
 };
 
 }  // namespace wprt

@@ -134,6 +134,11 @@ class Runtime:
         check(lib.wp_runtime_gemm_stats(self._h, C.byref(n), C.byref(fl), C.byref(sec)))
         return n.value, fl.value, sec.value
 
+    def gemm_report(self):
+        buf = C.create_string_buffer(1 << 16)
+        check(lib.wp_runtime_gemm_report(self._h, buf, len(buf)))
+        return buf.value.decode()
+
     # ----------------------------------------------------------- parameters
     def param_names(self):
         n = C.c_int()

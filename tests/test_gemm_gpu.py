@@ -127,3 +127,62 @@ def test_tc_large_throughput_sanity():
     M, N, K = 4096, 6144, 2048
     out, ref = run(M, N, K, False, False, torch.bfloat16, c_dtype=torch.float32)
     torch.testing.assert_close(out, ref, rtol=1e-3, atol=5e-2)
+
+
+def _raw(M, N, K, a, lda, a_mn, b, ldb, b_mn, c, causal, nb=1, ab=0, bb=0, cb=0, in_code=1, c_code=0):
+    fn = lib.wp_debug_gemm_causal
+    st = fn(M, N, K, nb, 1, in_code, a.data_ptr(), lda, int(a_mn), ab, 0, b.data_ptr(), ldb, int(b_mn), bb, 0,
+            0, 1.0, c.data_ptr(), c_code, N, cb, 0, None, None, None, causal)
+    assert st == 0, lib.wp_last_error().decode()
+    torch.cuda.synchronize()
+
+
+lib.wp_debug_gemm_causal.restype = C.c_int
+lib.wp_debug_gemm_causal.argtypes = lib.wp_debug_gemm.argtypes + [C.c_int]
+CAUSAL_SKIP_UPPER, CAUSAL_K_UP_TO_ROW, CAUSAL_K_FROM_ROW = 1, 2, 3
+
+
+def causal_p(s, nb, dtype):
+    """Lower-triangular 'probabilities' with NaN beyond each row's 128-wide
+    tile -- memory the causal GEMMs must never read."""
+    p = torch.rand(nb, s, s, device="cuda").tril()
+    q = torch.arange(s, device="cuda")[:, None]
+    j = torch.arange(s, device="cuda")[None, :]
+    p[:, (j >= (q // 128 + 1) * 128).expand(s, s)] = float("nan")
+    return p.to(dtype)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_causal_modes(dtype):
+    s, d, nb = 384, 128, 2
+    in_code = 1 if dtype == torch.bfloat16 else 0
+    q = torch.randn(nb, s, d, device="cuda").to(dtype)
+    k = torch.randn(nb, s, d, device="cuda").to(dtype)
+    # S = Q K^T with upper tiles skipped: lower triangle must match
+    c = torch.zeros(nb, s, s, device="cuda")
+    _raw(s, s, d, q, d, False, k, d, False, c, CAUSAL_SKIP_UPPER, nb, s * d, s * d, s * s, in_code)
+    ref = q.float() @ k.float().transpose(1, 2)
+    tri = torch.ones(s, s, device="cuda").tril().bool()
+    tol = 2e-2 if in_code else 1e-4
+    torch.testing.assert_close(c[:, tri], ref[:, tri], rtol=tol, atol=tol)
+    # O = P V reading keys only up to each row tile's end
+    p = causal_p(s, nb, dtype)
+    v = torch.randn(nb, s, d, device="cuda").to(dtype)
+    o = torch.zeros(nb, s, d, device="cuda")
+    _raw(s, d, s, p, s, False, v, d, True, o, CAUSAL_K_UP_TO_ROW, nb, s * s, s * d, s * d, in_code)
+    pz = torch.nan_to_num(p.float(), nan=0.0)
+    torch.testing.assert_close(o, pz @ v.float(), rtol=tol, atol=tol * 4)
+    # dV = P^T dO with queries starting at each key tile
+    do = torch.randn(nb, s, d, device="cuda").to(dtype)
+    dv = torch.zeros(nb, s, d, device="cuda")
+    _raw(s, d, s, p, s, True, do, d, True, dv, CAUSAL_K_FROM_ROW, nb, s * s, s * d, s * d, in_code)
+    torch.testing.assert_close(dv, pz.transpose(1, 2) @ do.float(), rtol=tol, atol=tol * 4)
+
+
+def test_tc_narrow_n_tile():
+    """N <= 128 selects the 128-wide tile; every layout."""
+    for a_mn, b_mn in LAYOUTS:
+        out, ref = run(384, 128, 320, a_mn, b_mn, torch.bfloat16, c_dtype=torch.float32)
+        torch.testing.assert_close(out, ref, rtol=1e-3, atol=2e-2)
+        out, ref = run(256, 72, 128, a_mn, b_mn, torch.bfloat16, c_dtype=torch.float32)
+        torch.testing.assert_close(out, ref, rtol=1e-3, atol=2e-2)
