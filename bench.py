@@ -5,7 +5,7 @@
 Workload (BASELINE.json configs[3]): GPT-1.3B-like (24 layers, hidden 2048,
 16 heads, ffn 8192, seq 1024, vocab 50304, tied embeddings), bf16 tensor-core
 compute with fp32 master weights and AdamW, Hanayo W=2 over P=N GPUs
-(N=1: all S=4 slices resident on one GPU), B=8 microbatches of 4 sequences,
+(N=1: all S=4 slices resident on one GPU), B=8 microbatches of 8 sequences,
 synthetic tokens (splitmix64), random-init weights.
 
 One "step" = one full synchronous training iteration: every microbatch's
@@ -197,7 +197,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="wavepipe", choices=["wavepipe", "reference"])
     ap.add_argument("--microbatches", type=int, default=8)
-    ap.add_argument("--mbs", type=int, default=4)
+    ap.add_argument("--mbs", type=int, default=8)
     ap.add_argument("--waves", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gemm-report", action="store_true", help="per-shape GEMM table on stderr")

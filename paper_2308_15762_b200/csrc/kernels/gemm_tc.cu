@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty_bar[a], 8);  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
-    const int ew = warp & 3;  // TMEM lane quarter this warp may access
+    const int ew = warp & 3;          // TMEM lane quarter this warp may access
+    const int half = (warp - 4) >> 2;  // which half of the tile's columns
     int local = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       int mb, nb, z1, z2, kb0, kb1;
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int64_t zoff = static_cast<int64_t>(z1) * p.epi.c_b1 + static_cast<int64_t>(z2) * p.epi.c_b2;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * 256;
       const int col_end = min(BN, p.N - nb * BN);
-      for (int c = 0; c < col_end; c += 32) {
+      for (int c = half * (BN / 2); c < min(col_end, (half + 1) * (BN / 2)); c += 32) {
         float v[32];
         tmem_ld32(taddr + c, v);  // warp-collective: every lane participates
         if (row < p.M) epilogue_chunk(p, v, row, nb * BN + c, zoff);
@@ -265,7 +266,7 @@ void fill_params(const GemmProblem& g, Params& p, int tile_m, int tile_n) {
   const int es = g.epi.c_dtype == kF32 ? 4 : 2;
   auto al = [&](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
   p.vec_ok = (g.epi.ldc * es) % 16 == 0 && (g.epi.c_b1 * es) % 16 == 0 && (g.epi.c_b2 * es) % 16 == 0 &&
-             al(g.epi.c) && al(g.epi.resid) && al(g.epi.aux);
+             al(g.epi.c) && al(g.epi.resid) && al(g.epi.aux) && al(g.epi.bias);
 }
 
 }  // namespace tc

@@ -58,7 +58,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+      mbar_init(&tempty_bar[a], 16);  // 8 epilogue warps x 2 CTAs (leader's copy is used)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -142,6 +142,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp & 3;
+    const int half = (warp - 4) >> 2;
     int local = 0;
     for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
       int mb, nb, z1, z2;
@@ -154,7 +155,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int64_t zoff = static_cast<int64_t>(z1) * p.epi.c_b1 + static_cast<int64_t>(z2) * p.epi.c_b2;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * PBN;
       const int col_end = min(PBN, p.N - nb * PBN);
-      for (int c = 0; c < col_end; c += 32) {
+      for (int c = half * (PBN / 2); c < min(col_end, (half + 1) * (PBN / 2)); c += 32) {
         float v[32];
         tmem_ld32(taddr + c, v);
         if (row < p.M) epilogue_chunk(p, v, row, nb * PBN + c, zoff);

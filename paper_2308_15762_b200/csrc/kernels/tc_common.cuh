@@ -17,7 +17,7 @@ namespace tc {
 constexpr int BM = 128, BK = 64;
 constexpr int A_BYTES = BM * BK * 2;      // 16 KB
 constexpr int CHUNK_BYTES = 64 * BK * 2;  // one 64(MN) x 64(K) SW128 box, 8 KB
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 384;  // warps 0-3 control, 4-11 epilogue (two column halves)
 constexpr int TMEM_COLS = 512;
 
 // Tile width N: 256 for the linear layers, 128 when N <= 128 (attention's
@@ -151,93 +151,127 @@ __device__ __forceinline__ void store_elem(void* base, int dtype, int64_t off, f
   else static_cast<__nv_bfloat16*>(base)[off] = __float2bfloat16_rn(v);
 }
 
-// Epilogue for one row segment of 32 columns starting at (row, col0).
+// 8 contiguous elements of C-typed memory <-> floats (16 B bf16 / 32 B fp32).
+__device__ __forceinline__ void ld8(const void* base, int dtype, int64_t off, float* v) {
+  if (dtype == kF32) {
+    const float4 a = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + off);
+    const float4 b = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + off + 4);
+    v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+  } else {
+    const uint4 u = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      v[2 * i] = f.x, v[2 * i + 1] = f.y;
+    }
+  }
+}
+
+__device__ __forceinline__ void st8(void* base, int dtype, int64_t off, const float* v) {
+  if (dtype == kF32) {
+    float* c = static_cast<float*>(base) + off;
+    *reinterpret_cast<float4*>(c) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(c + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(base) + off) = u;
+  }
+}
+
+// GELU (tanh form) on the MUFU tanh: the tensor-core path runs in bf16 mode,
+// whose 2^-9 storage rounding dominates tanh.approx's ~2^-11 error.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_fast(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.0f + tanh_fast(k0 * fmaf(k1 * x, x * x, x)));
+}
+__device__ __forceinline__ float gelu_grad_fast(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float x2 = x * x;
+  const float t = tanh_fast(k0 * fmaf(k1 * x, x2, x));
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * fmaf(3.0f * k1, x2, 1.0f);
+}
+
+__device__ __forceinline__ float round_to(int dtype, float x) {
+  return dtype == kF32 ? x : __bfloat162float(__float2bfloat16_rn(x));
+}
+
+// Epilogue of one row segment of 32 accumulator columns at (row, col0).
+// Full, aligned segments move 8 elements per access; ragged tails go scalar.
 __device__ __forceinline__ void epilogue_chunk(const Params& p, const float* acc, int row, int col0,
                                                int64_t zoff) {
   const Epilogue& e = p.epi;
   const int64_t base = zoff + static_cast<int64_t>(row) * e.ldc + col0;
   const int ncols = min(32, p.N - col0);
-  float v[32];
+  const int dt = e.mode == kEpiAccum ? kF32 : e.c_dtype;
+  if (p.vec_ok && ncols == 32) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = acc[i] * e.alpha;
-  if (e.bias) {
+    for (int g = 0; g < 4; ++g) {
+      float v[8];
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < ncols) v[i] += e.bias[col0 + i];
-  }
-  const bool vec = p.vec_ok && ncols == 32;
-  if (e.mode == kEpiAccum) {  // fp32 C
-    float* c = static_cast<float*>(e.c) + base;
-    if (vec) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        float4 o = *reinterpret_cast<float4*>(c + i);
-        o.x += v[i];
-        o.y += v[i + 1];
-        o.z += v[i + 2];
-        o.w += v[i + 3];
-        *reinterpret_cast<float4*>(c + i) = o;
+      for (int i = 0; i < 8; ++i) v[i] = acc[8 * g + i] * e.alpha;
+      if (e.bias) {
+        const float4 b0 = *reinterpret_cast<const float4*>(e.bias + col0 + 8 * g);
+        const float4 b1 = *reinterpret_cast<const float4*>(e.bias + col0 + 8 * g + 4);
+        v[0] += b0.x, v[1] += b0.y, v[2] += b0.z, v[3] += b0.w, v[4] += b1.x, v[5] += b1.y, v[6] += b1.z,
+            v[7] += b1.w;
       }
-    } else {
+      const int64_t off = base + 8 * g;
+      if (e.mode == kEpiAccum) {
+        float o[8];
+        ld8(e.c, kF32, off, o);
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (i < ncols) c[i] += v[i];
+        for (int i = 0; i < 8; ++i) v[i] += o[i];
+      } else if (e.mode == kEpiResidual) {
+        float r[8];
+        ld8(e.resid, dt, off, r);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] += r[i];
+      } else if (e.mode == kEpiGelu) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = round_to(dt, v[i]);  // GELU of the stored pre-activation
+        st8(e.aux, dt, off, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = gelu_fast(v[i]);
+      } else if (e.mode == kEpiDGelu) {
+        float u[8];
+        ld8(e.aux, dt, off, u);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_fast(u[i]);
+      }
+      st8(e.c, dt, off, v);
     }
     return;
   }
-  if (e.mode == kEpiResidual) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < ncols) v[i] += load_elem(e.resid, e.c_dtype, base + i);
-  } else if (e.mode == kEpiGelu) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if (i < ncols) {
-        // GELU of the pre-activation as stored, so backward sees the same value.
-        const float pre = e.c_dtype == kF32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
-        store_elem(e.aux, e.c_dtype, base + i, pre);
-        v[i] = gelu_f(pre);
-      }
+  for (int i = 0; i < 32; ++i) {
+    if (i >= ncols) continue;
+    const int64_t off = base + i;
+    float v = acc[i] * e.alpha + (e.bias ? e.bias[col0 + i] : 0.f);
+    if (e.mode == kEpiAccum) {
+      static_cast<float*>(e.c)[off] += v;
+      continue;
     }
-  } else if (e.mode == kEpiDGelu) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < ncols) v[i] *= gelu_grad_f(load_elem(e.aux, e.c_dtype, base + i));
-  }
-  if (e.c_dtype == kBF16) {
-    __nv_bfloat16* c = static_cast<__nv_bfloat16*>(e.c) + base;
-    if (vec) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 pk;
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[i], v[i + 1]);
-        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]);
-        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
-        pk.x = *reinterpret_cast<uint32_t*>(&h0);
-        pk.y = *reinterpret_cast<uint32_t*>(&h1);
-        pk.z = *reinterpret_cast<uint32_t*>(&h2);
-        pk.w = *reinterpret_cast<uint32_t*>(&h3);
-        *reinterpret_cast<uint4*>(c + i) = pk;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (i < ncols) c[i] = __float2bfloat16_rn(v[i]);
+    if (e.mode == kEpiResidual) {
+      v += load_elem(e.resid, dt, off);
+    } else if (e.mode == kEpiGelu) {
+      v = round_to(dt, v);
+      store_elem(e.aux, dt, off, v);
+      v = gelu_fast(v);
+    } else if (e.mode == kEpiDGelu) {
+      v *= gelu_grad_fast(load_elem(e.aux, dt, off));
     }
-  } else {
-    float* c = static_cast<float*>(e.c) + base;
-    if (vec) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (i < ncols) c[i] = v[i];
-    }
+    store_elem(e.c, dt, off, v);
   }
 }
-
 
 // --- CTA-pair (cta_group::2) variants -------------------------------------
 // TMA load whose completion is counted on the pair leader's mbarrier (the

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -380,7 +381,249 @@ float* Runtime::grad(DeviceState& d, const std::string& name) const {
   return d.grad + d.params[it->second].offset;
 }
 
+namespace {
+
+// Debugging aid (WP_DEBUG_CHECK_GEMM=1): recompute sampled outputs of every
+// GEMM on the host from the device operands and report the first mismatch.
+float host_elem(const std::vector<uint16_t>& h, const std::vector<float>& f, int dtype, int64_t i) {
+  if (dtype == wpk::kF32) return f[i];
+  uint32_t u = static_cast<uint32_t>(h[i]) << 16;
+  float x;
+  std::memcpy(&x, &u, 4);
+  return x;
+}
+
+struct HostBuf {
+  std::vector<uint16_t> h;
+  std::vector<float> f;
+  int dtype;
+  void fetch(const void* p, int64_t n, int dt) {
+    dtype = dt;
+    if (dt == wpk::kF32) {
+      f.resize(n);
+      cudaMemcpy(f.data(), p, n * 4, cudaMemcpyDeviceToHost);
+    } else {
+      h.resize(n);
+      cudaMemcpy(h.data(), p, n * 2, cudaMemcpyDeviceToHost);
+    }
+  }
+  float at(int64_t i) const { return host_elem(h, f, dtype, i); }
+};
+
+int64_t operand_extent(const wpk::Operand& o, int rows, int K, int nb1, int nb2) {
+  const int64_t inner = o.mn_major ? static_cast<int64_t>(K - 1) * o.ld + rows : static_cast<int64_t>(rows - 1) * o.ld + K;
+  return inner + static_cast<int64_t>(nb1 - 1) * o.b1 + static_cast<int64_t>(nb2 - 1) * o.b2;
+}
+
+void check_gemm(const wpk::GemmProblem& g, cudaStream_t s, const std::function<void()>& run) {
+  const int cdt = g.epi.mode == wpk::kEpiAccum ? wpk::kF32 : g.epi.c_dtype;
+  const int64_t c_ext = static_cast<int64_t>(g.M - 1) * g.epi.ldc + g.N +
+                        static_cast<int64_t>(g.nb1 - 1) * g.epi.c_b1 + static_cast<int64_t>(g.nb2 - 1) * g.epi.c_b2;
+  cudaStreamSynchronize(s);
+  HostBuf A, B, C0, R, X;
+  A.fetch(g.A.ptr, operand_extent(g.A, g.M, g.K, g.nb1, g.nb2), g.in_dtype);
+  B.fetch(g.B.ptr, operand_extent(g.B, g.N, g.K, g.nb1, g.nb2), g.in_dtype);
+  if (g.epi.mode == wpk::kEpiAccum) C0.fetch(g.epi.c, c_ext, cdt);
+  if (g.epi.mode == wpk::kEpiResidual) R.fetch(g.epi.resid, c_ext, cdt);
+  if (g.epi.mode == wpk::kEpiDGelu) X.fetch(g.epi.aux, c_ext, cdt);
+  std::vector<float> bias;
+  if (g.epi.bias) {
+    bias.resize(g.N);
+    cudaMemcpy(bias.data(), g.epi.bias, g.N * 4, cudaMemcpyDeviceToHost);
+  }
+  run();
+  cudaStreamSynchronize(s);
+  HostBuf C;
+  C.fetch(g.epi.c, c_ext, cdt);
+  uint64_t rng = 88172645463325252ull;
+  auto rnd = [&](int n) {
+    rng ^= rng << 13, rng ^= rng >> 7, rng ^= rng << 17;
+    return static_cast<int>(rng % static_cast<uint64_t>(n));
+  };
+  auto gelu = [](double x) { return 0.5 * x * (1 + std::tanh(0.7978845608028654 * (x + 0.044715 * x * x * x))); };
+  auto dgelu = [](double x) {
+    const double t = std::tanh(0.7978845608028654 * (x + 0.044715 * x * x * x));
+    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x * x);
+  };
+  const int64_t total = int64_t(g.M) * g.N * g.nb1 * g.nb2;
+  const bool full = total * g.K <= 40000000;
+  const int64_t iters = full ? total : 4096;
+  int64_t bad = 0;
+  for (int64_t it = 0; it < iters; ++it) {
+    int z1, z2, m, n;
+    if (full) {
+      int64_t r = it;
+      n = static_cast<int>(r % g.N), r /= g.N;
+      m = static_cast<int>(r % g.M), r /= g.M;
+      z1 = static_cast<int>(r % g.nb1), z2 = static_cast<int>(r / g.nb1);
+    } else {
+      z1 = rnd(g.nb1), z2 = rnd(g.nb2), m = rnd(g.M), n = rnd(g.N);
+    }
+    if (g.causal == wpk::kCausalSkipUpper && n > m) continue;
+    int k0 = 0, k1 = g.K;
+    if (g.causal == wpk::kCausalKUpToRow) k1 = std::min(g.K, (m / 128 + 1) * 128);
+    if (g.causal == wpk::kCausalKFromRow) k0 = (m / 128) * 128;
+    double acc = 0, mag = 0;
+    for (int k = k0; k < k1; ++k) {
+      const int64_t ai = z1 * g.A.b1 + z2 * g.A.b2 + (g.A.mn_major ? int64_t(k) * g.A.ld + m : int64_t(m) * g.A.ld + k);
+      const int64_t bi = z1 * g.B.b1 + z2 * g.B.b2 + (g.B.mn_major ? int64_t(k) * g.B.ld + n : int64_t(n) * g.B.ld + k);
+      const double pr = double(A.at(ai)) * double(B.at(bi));
+      acc += pr;
+      mag += std::fabs(pr);
+    }
+    const int64_t ci = z1 * g.epi.c_b1 + z2 * g.epi.c_b2 + int64_t(m) * g.epi.ldc + n;
+    double want = acc * g.epi.alpha + (g.epi.bias ? bias[n] : 0.0);
+    double tol_scale = mag * std::fabs(g.epi.alpha) + (g.epi.bias ? std::fabs(bias[n]) : 0.0);
+    switch (g.epi.mode) {
+      case wpk::kEpiAccum: want += C0.at(ci); tol_scale += std::fabs(C0.at(ci)); break;
+      case wpk::kEpiResidual: want += R.at(ci); tol_scale += std::fabs(R.at(ci)); break;
+      case wpk::kEpiGelu: want = gelu(want); break;
+      case wpk::kEpiDGelu: want *= dgelu(X.at(ci)); tol_scale *= 1.2; break;
+      default: break;
+    }
+    const double got = C.at(ci);
+    // bf16 x bf16 products are exact in fp32; fp32 accumulation error ~K ulps of
+    // sum|p|; a bf16 output adds one rounding (2^-9 relative).
+    const double tol = 1e-7 + 2e-5 * tol_scale + (cdt == wpk::kF32 ? 1e-6 : 8e-3) * std::fabs(want);
+    if (!(std::fabs(got - want) <= tol) && bad++ < 3) {
+      std::fprintf(stderr,
+                   "GEMM CHECK FAILED: M=%d N=%d K=%d nb=%dx%d A_mn=%d B_mn=%d mode=%d causal=%d c_dtype=%d at "
+                   "z=(%d,%d) m=%d n=%d: got %.6g want %.6g (tol %.3g)\n",
+                   g.M, g.N, g.K, g.nb1, g.nb2, int(g.A.mn_major), int(g.B.mn_major), g.epi.mode, g.causal,
+                   g.epi.c_dtype, z1, z2, m, n, got, want, tol);
+    }
+  }
+  if (bad) std::fprintf(stderr, "GEMM CHECK: %lld of %lld checked outputs wrong\n", (long long)bad, (long long)iters);
+}
+
+bool check_ops_enabled() {
+  static const bool on = std::getenv("WP_DEBUG_CHECK_OPS") != nullptr;  // debugging aid
+  return on;
+}
+
+void report(const char* what, int64_t bad, int64_t n, double worst) {
+  if (bad) std::fprintf(stderr, "OP CHECK %s: %lld of %lld wrong (worst %.3g)\n", what, (long long)bad, (long long)n, worst);
+}
+
+void check_layernorm(int dt, const void* x, const float* w, const float* b, const void* y, const float* mean,
+                     const float* rstd, int T, int h, cudaStream_t s) {
+  cudaStreamSynchronize(s);
+  HostBuf X, Y, W, Bb, Mu, Rs;
+  X.fetch(x, int64_t(T) * h, dt);
+  Y.fetch(y, int64_t(T) * h, dt);
+  W.fetch(w, h, wpk::kF32);
+  Bb.fetch(b, h, wpk::kF32);
+  Mu.fetch(mean, T, wpk::kF32);
+  Rs.fetch(rstd, T, wpk::kF32);
+  int64_t bad = 0;
+  double worst = 0;
+  for (int t = 0; t < T; ++t) {
+    double mu = 0, var = 0;
+    for (int c = 0; c < h; ++c) mu += X.at(int64_t(t) * h + c);
+    mu /= h;
+    for (int c = 0; c < h; ++c) var += (X.at(int64_t(t) * h + c) - mu) * (X.at(int64_t(t) * h + c) - mu);
+    const double rs = 1.0 / std::sqrt(var / h + 1e-5);
+    for (int c = 0; c < h; ++c) {
+      const double want = (X.at(int64_t(t) * h + c) - mu) * rs * W.at(c) + Bb.at(c);
+      const double err = std::fabs(Y.at(int64_t(t) * h + c) - want);
+      if (err > 1e-2 * (1 + std::fabs(want))) ++bad, worst = std::max(worst, err);
+    }
+    if (std::fabs(Mu.at(t) - mu) > 1e-3 * (1 + std::fabs(mu))) ++bad;
+  }
+  report("layernorm_fwd", bad, int64_t(T) * h, worst);
+}
+
+// LayerNorm backward: dx vs host, and the dw/db increments.
+struct LnBwdCheck {
+  HostBuf DY, X, MU, RS, W, R, DW0, DB0;
+  int dt, T, h;
+  bool has_res;
+  void before(int dt_, const void* dy, const void* x, const float* mean, const float* rstd, const float* w,
+              const void* dres, const float* dw, const float* db, int T_, int h_, cudaStream_t s) {
+    cudaStreamSynchronize(s);
+    dt = dt_, T = T_, h = h_, has_res = dres != nullptr;
+    DY.fetch(dy, int64_t(T) * h, dt);
+    X.fetch(x, int64_t(T) * h, dt);
+    MU.fetch(mean, T, wpk::kF32);
+    RS.fetch(rstd, T, wpk::kF32);
+    W.fetch(w, h, wpk::kF32);
+    if (has_res) R.fetch(dres, int64_t(T) * h, dt);
+    DW0.fetch(dw, h, wpk::kF32);
+    DB0.fetch(db, h, wpk::kF32);
+  }
+  void after(const void* dx, const float* dw, const float* db, cudaStream_t s) {
+    cudaStreamSynchronize(s);
+    HostBuf DX, DW, DB;
+    DX.fetch(dx, int64_t(T) * h, dt);
+    DW.fetch(dw, h, wpk::kF32);
+    DB.fetch(db, h, wpk::kF32);
+    std::vector<double> gw(h, 0), gb(h, 0);
+    int64_t bad = 0;
+    double worst = 0;
+    for (int t = 0; t < T; ++t) {
+      double sg = 0, sgx = 0;
+      for (int c = 0; c < h; ++c) {
+        const int64_t i = int64_t(t) * h + c;
+        const double xh = (X.at(i) - MU.at(t)) * RS.at(t), g = DY.at(i) * W.at(c);
+        sg += g, sgx += g * xh;
+        gw[c] += DY.at(i) * xh, gb[c] += DY.at(i);
+      }
+      sg /= h, sgx /= h;
+      for (int c = 0; c < h; ++c) {
+        const int64_t i = int64_t(t) * h + c;
+        const double xh = (X.at(i) - MU.at(t)) * RS.at(t);
+        const double want = RS.at(t) * (DY.at(i) * W.at(c) - sg - xh * sgx) + (has_res ? R.at(i) : 0.0);
+        const double err = std::fabs(DX.at(i) - want);
+        if (err > 1e-2 * std::fabs(want) + 1e-3 * RS.at(t) * std::fabs(sg) + 1e-7) ++bad, worst = std::max(worst, err);
+      }
+    }
+    report("layernorm_bwd dx", bad, int64_t(T) * h, worst);
+    bad = 0, worst = 0;
+    for (int c = 0; c < h; ++c) {
+      const double ew = std::fabs(DW.at(c) - DW0.at(c) - gw[c]), eb = std::fabs(DB.at(c) - DB0.at(c) - gb[c]);
+      if (ew > 1e-4 * std::fabs(gw[c]) + 1e-7 || eb > 1e-4 * std::fabs(gb[c]) + 1e-7) ++bad, worst = std::max(worst, std::max(ew, eb));
+    }
+    report("layernorm_bwd dw/db", bad, h, worst);
+  }
+};
+
+void check_softmax(int dt, const float* S, const void* P, int rows, int n, int causal, cudaStream_t s) {
+  cudaStreamSynchronize(s);
+  HostBuf Sh, Ph;
+  Sh.fetch(S, int64_t(rows) * n, wpk::kF32);
+  Ph.fetch(P, int64_t(rows) * n, dt);
+  int64_t bad = 0;
+  double worst = 0;
+  for (int r = 0; r < rows; ++r) {
+    const int q = r % n, valid = causal ? q + 1 : n;
+    double m = -1e300, sum = 0;
+    for (int j = 0; j < valid; ++j) m = std::max(m, double(Sh.at(int64_t(r) * n + j)));
+    for (int j = 0; j < valid; ++j) sum += std::exp(Sh.at(int64_t(r) * n + j) - m);
+    for (int j = 0; j < valid; ++j) {
+      const double want = std::exp(Sh.at(int64_t(r) * n + j) - m) / sum;
+      const double err = std::fabs(Ph.at(int64_t(r) * n + j) - want);
+      if (err > 1e-2 * want + 1e-6) ++bad, worst = std::max(worst, err);
+    }
+  }
+  report("softmax_fwd", bad, int64_t(rows) * n, worst);
+}
+
+
+}  // namespace
+
 void Runtime::gemm(DeviceState& d, const wpk::GemmProblem& g) {
+  static const bool check = std::getenv("WP_DEBUG_CHECK_GEMM") != nullptr;  // debugging aid
+  if (check) {
+    check_gemm(g, d.compute, [&] { launches_ += wpk::gemm(g, d.compute); });
+    return;
+  }
+  static const bool sync_each = std::getenv("WP_DEBUG_SYNC_GEMM") != nullptr;  // debugging aid
+  if (sync_each) {
+    ck(cudaStreamSynchronize(d.compute), "debug sync");
+    launches_ += wpk::gemm(g, d.compute);
+    ck(cudaStreamSynchronize(d.compute), "debug sync");
+    return;
+  }
   if (!profiling_) {
     launches_ += wpk::gemm(g, d.compute);
     return;
@@ -440,6 +683,9 @@ BufPtr Runtime::unit_fwd(DeviceState& d, int ui, int mb, BufPtr x, UnitStash& st
   const std::string lnname = u.kind == UnitKind::Head ? "lnf" : L + lnw;
   launches_ += wpk::layernorm_fwd(dt, x->p, master(d, lnname + ".w"), master(d, lnname + ".b"), st.ln->p,
                                   static_cast<float*>(st.mean->p), static_cast<float*>(st.rstd->p), T, h, cs);
+  if (check_ops_enabled())
+    check_layernorm(dt, x->p, master(d, lnname + ".w"), master(d, lnname + ".b"), st.ln->p,
+                    static_cast<float*>(st.mean->p), static_cast<float*>(st.rstd->p), T, h, cs);
   wpk::GemmProblem g;
   g.in_dtype = dt;
   if (u.kind == UnitKind::Attn) {
@@ -461,6 +707,7 @@ BufPtr Runtime::unit_fwd(DeviceState& d, int ui, int mb, BufPtr x, UnitStash& st
     gemm(d, sg);
     st.b = act(int64_t(m_.mbs) * H * S * S);  // P
     launches_ += wpk::softmax_fwd(dt, d.scores, st.b->p, m_.mbs * H * S, S, m_.causal, cs);
+    if (check_ops_enabled()) check_softmax(dt, d.scores, st.b->p, m_.mbs * H * S, S, m_.causal, cs);
     // ctx = P V
     st.c = act(int64_t(T) * h);
     wpk::GemmProblem pv;
@@ -555,10 +802,16 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   };
   auto ln_bwd = [&](const BufPtr& dln, const std::string& name, const BufPtr& dres) {
     BufPtr dx = act(int64_t(T) * h);
+    LnBwdCheck chk;
+    if (check_ops_enabled())
+      chk.before(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p), static_cast<float*>(st.rstd->p),
+                 master(d, name + ".w"), dres ? dres->p : nullptr, grad(d, name + ".w"), grad(d, name + ".b"), T, h,
+                 cs);
     launches_ += wpk::layernorm_bwd(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p),
                                     static_cast<float*>(st.rstd->p), master(d, name + ".w"),
                                     dres ? dres->p : nullptr, dx->p, grad(d, name + ".w"), grad(d, name + ".b"), T, h,
                                     cs);
+    if (check_ops_enabled()) chk.after(dx->p, grad(d, name + ".w"), grad(d, name + ".b"), cs);
     return dx;
   };
 
@@ -973,11 +1226,14 @@ void Runtime::set_param(const std::string& name, const float* host, int64_t n) {
   DevGuard g(d.cuda);
   ck(cudaDeviceSynchronize(), "sync");
   const int64_t off = d.params[it->second.slot].offset;
-  ck(cudaMemcpy(d.master + off, host, n * sizeof(float), cudaMemcpyHostToDevice), "param H2D");
+  // Stream-ordered copy: a plain cudaMemcpy from pageable memory may return
+  // before its DMA lands, and the compute stream (non-blocking) would not
+  // order the shadow cast after it.
+  ck(cudaMemcpyAsync(d.master + off, host, n * sizeof(float), cudaMemcpyHostToDevice, d.compute), "param H2D");
   if (d.shadow) {
     launches_ += wpk::cast_f32_to_bf16(d.master + off, static_cast<__nv_bfloat16*>(d.shadow) + off, n, d.compute);
-    ck(cudaStreamSynchronize(d.compute), "sync");
   }
+  ck(cudaStreamSynchronize(d.compute), "sync");
 }
 
 }  // namespace wprt
