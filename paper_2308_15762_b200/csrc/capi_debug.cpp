@@ -60,3 +60,34 @@ extern "C" int wp_debug_gemm_causal(int M, int N, int K, int nb1, int nb2, int i
   return debug_gemm(M, N, K, nb1, nb2, in_dtype, a, lda, a_mn, a_b1, a_b2, b, ldb, b_mn, b_b1, b_b2, mode, alpha, c,
                     c_dtype, ldc, c_b1, c_b2, bias, resid, aux, causal);
 }
+
+#include "kernels/attention.cuh"
+
+extern "C" int wp_debug_flash_fwd(int mbs, int seq, int heads, int head_dim, int causal, const void* qkv, void* ctx,
+                                  float* lse2) {
+  try {
+    wpk::AttnShape s{mbs, seq, heads, head_dim, heads * head_dim, causal};
+    wpk::flash_attn_fwd(s, qkv, ctx, lse2, nullptr);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return wpc::fail(WP_ERR_CUDA, std::string("flash fwd: ") + cudaGetErrorString(e));
+    return WP_OK;
+  } catch (...) {
+    return wpc::map_exception();
+  }
+}
+
+extern "C" int wp_debug_flash_bwd(int mbs, int seq, int heads, int head_dim, int causal, const void* qkv,
+                                  const void* out, const void* dout, const float* lse2, float* delta, float* dq_acc,
+                                  void* dqkv) {
+  try {
+    wpk::AttnShape s{mbs, seq, heads, head_dim, heads * head_dim, causal};
+    wpk::flash_attn_bwd(s, qkv, out, dout, lse2, delta, dq_acc, dqkv, nullptr);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return wpc::fail(WP_ERR_CUDA, std::string("flash bwd: ") + cudaGetErrorString(e));
+    return WP_OK;
+  } catch (...) {
+    return wpc::map_exception();
+  }
+}

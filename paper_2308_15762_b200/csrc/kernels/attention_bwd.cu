@@ -1,0 +1,413 @@
+// Flash attention backward on the 5th-gen tensor cores (sm_100a).
+//
+// One CTA per (128-key tile j, head, sequence); K_j and V_j stay in shared
+// memory while the query tiles i (causal: i >= j) stream through.  Per q tile:
+//   MMA        S^T  = K_j Q_i^T      (M=keys, N=queries, K=D)   -> TMEM
+//              dP^T = V_j dO_i^T     (M=keys, N=queries, K=D)   -> TMEM
+//   softmax    4 warps, one key row per thread:  P^T = 2^(t - lse2),
+//              dS^T = P^T * (dP^T - Delta) / sqrt(D)  -> bf16 -> smem (SW128)
+//   MMA        dV_j += P^T dO_i,  dK_j += dS^T Q_i        (TMEM accumulators)
+//              dQ_i  = dS K_j     (A = the dS^T tile read MN-major)
+//   dQ warps   4 warps drain dQ_i from TMEM with red.global.add.v4.f32 into an
+//              fp32 accumulator (every key tile contributes to each q tile)
+// Delta = rowsum(dO * O) comes from attn_bwd_prep; dq_finish converts the fp32
+// dQ accumulator to bf16 into dqkv.  dK, dV are written at the end.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "kernels/attention.cuh"
+#include "kernels/tc_common.cuh"
+
+namespace wpk {
+namespace {
+
+using namespace tc;
+
+constexpr int T128 = 128;
+constexpr int ATOM = 128 * 64 * 2;  // SW128 atom: 128 rows x 64 bf16
+constexpr int BW_THREADS = 384;     // warps 0-3 control, 4-7 softmax, 8-11 dQ drain
+constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256;
+
+template <int D>
+struct BwCfg {
+  static constexpr int TILE = T128 * D * 2;     // K, V, Q, dO tiles
+  static constexpr int PT = T128 * T128 * 2;    // P^T / dS^T tiles
+  static constexpr int SMEM = 4 * TILE + 2 * PT + 2 * 2 * T128 * 4 + 1024 + 256;
+  static constexpr uint32_t kColDK = kColDV + D;
+};
+
+struct BwParams {
+  int seq, heads, n_tiles, causal, hidden;
+  float scale_log2, scale;
+  const float* lse2;
+  const float* delta;
+  float* dq_acc;                // [T, h] fp32
+  __nv_bfloat16* dqkv;          // [T, 3h]
+};
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t swz(int r, int c) {  // 16-B chunk c of row r, SW128 K-major atoms
+  const int atom = c >> 3, cc = c & 7;
+  return atom * ATOM + (r >> 3) * 1024 + (r & 7) * 128 + ((cc ^ (r & 7)) << 4);
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(BW_THREADS, 1)
+    flash_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                     const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
+                     const __grid_constant__ BwParams p) {
+  using Cfg = BwCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + Cfg::TILE;
+  uint8_t* sQ = sV + Cfg::TILE;
+  uint8_t* sDO = sQ + Cfg::TILE;
+  uint8_t* sP = sDO + Cfg::TILE;  // P^T  [keys x queries]
+  uint8_t* sDS = sP + Cfg::PT;    // dS^T [keys x queries]
+  float* sLse = reinterpret_cast<float*>(sDS + Cfg::PT);  // [2][128]
+  float* sDelta = sLse + 2 * T128;                        // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDelta + 2 * T128);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* qdo_full = bars + 1;
+  uint64_t* qdo_empty = bars + 2;
+  uint64_t* s_full = bars + 3;
+  uint64_t* ds_full = bars + 4;
+  uint64_t* pds_free = bars + 5;
+  uint64_t* dq_full = bars + 6;
+  uint64_t* dq_free = bars + 7;
+  uint64_t* dkv_done = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kj = static_cast<int>(blockIdx.x % p.n_tiles);  // light-to-heavy order reversed: small kj = most q tiles
+  const int head = static_cast<int>((blockIdx.x / p.n_tiles) % p.heads);
+  const int b = static_cast<int>(blockIdx.x / (p.n_tiles * p.heads));
+  const int i0 = p.causal ? kj : 0;
+  const int n_it = p.n_tiles - i0;
+
+  if (warp == 0 && lane == 0) {
+    for (const CUtensorMap* m : {&map_q, &map_k, &map_v, &map_do})
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(kv_full, 1);
+    mbar_init(qdo_full, 1);
+    mbar_init(qdo_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(ds_full, 4);
+    mbar_init(pds_free, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_free, 4);
+    mbar_init(dkv_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, 2 * Cfg::TILE);
+#pragma unroll
+      for (int a = 0; a < D / 64; ++a) {
+        tma_load_4d(&map_k, kv_full, sK + a * ATOM, a * 64, head, kj * T128, b);
+        tma_load_4d(&map_v, kv_full, sV + a * ATOM, a * 64, head, kj * T128, b);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int qi = i0 + it;
+        if (it > 0) mbar_wait(qdo_empty, (it - 1) & 1);
+        mbar_expect_tx(qdo_full, 2 * Cfg::TILE);
+#pragma unroll
+        for (int a = 0; a < D / 64; ++a) {
+          tma_load_4d(&map_q, qdo_full, sQ + a * ATOM, a * 64, head, qi * T128, b);
+          tma_load_4d(&map_do, qdo_full, sDO + a * ATOM, a * 64, head, qi * T128, b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // M=128 N=128 K-major/K-major (S^T, dP^T); M=128 N=D K-major A / MN-major B (dV, dK);
+      // M=128 N=D MN-major A / MN-major B (dQ).
+      constexpr uint32_t id_ss = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(T128 >> 3) << 17) |
+                                 (uint32_t(T128 >> 4) << 24);
+      constexpr uint32_t id_kv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) |
+                                 (uint32_t(T128 >> 4) << 24);
+      constexpr uint32_t id_dq = id_kv | (1u << 15);
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aDO = smem_u32(sDO);
+      const uint32_t aP = smem_u32(sP), aDS = smem_u32(sDS);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_it; ++it) {
+        mbar_wait(qdo_full, it & 1);
+        tc_fence_after();
+        // S^T = K Q^T, dP^T = V dO^T (reduction over D)
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * ATOM + (k & 3) * 32;
+          tc_mma(tmem + kColS, make_desc(aK + off, 16, 1024), make_desc(aQ + off, 16, 1024), id_ss, k != 0);
+        }
+        if (it > 0) {
+          mbar_wait(dq_free, (it - 1) & 1);  // dQ_{it-1} drained from the dP columns
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * ATOM + (k & 3) * 32;
+          tc_mma(tmem + kColDP, make_desc(aV + off, 16, 1024), make_desc(aDO + off, 16, 1024), id_ss, k != 0);
+        }
+        tc_commit(s_full);
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+        // dV += P^T dO, dK += dS^T Q (reduction over the 128 queries)
+#pragma unroll
+        for (int k = 0; k < T128 / 16; ++k) {
+          const uint32_t offa = (k >> 2) * ATOM + (k & 3) * 32;
+          tc_mma(tmem + kColDV, make_desc(aP + offa, 16, 1024), make_desc(aDO + k * 2048, ATOM, 1024), id_kv,
+                 (it | k) != 0);
+          tc_mma(tmem + Cfg::kColDK, make_desc(aDS + offa, 16, 1024), make_desc(aQ + k * 2048, ATOM, 1024), id_kv,
+                 (it | k) != 0);
+        }
+        tc_commit(qdo_empty);
+        // dQ = dS K (reduction over the 128 keys; dS^T tile read M-major)
+#pragma unroll
+        for (int k = 0; k < T128 / 16; ++k) {
+          tc_mma(tmem + kColDP, make_desc(aDS + k * 2048, ATOM, 1024), make_desc(aK + k * 2048, ATOM, 1024), id_dq,
+                 k != 0);
+        }
+        tc_commit(dq_full);
+        tc_commit(pds_free);
+      }
+      tc_commit(dkv_done);
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // -------------------------------------------------- P^T / dS^T (key rows)
+    const int ew = warp & 3;
+    const int r = ew * 32 + lane;
+    const uint32_t lb = static_cast<uint32_t>(ew * 32) << 16;
+    for (int it = 0; it < n_it; ++it) {
+      const int qi = i0 + it;
+      float* lse = sLse + (it & 1) * T128;
+      float* dl = sDelta + (it & 1) * T128;
+      const int64_t vec = (static_cast<int64_t>(b) * p.heads + head) * p.seq + qi * T128;
+      lse[r] = p.lse2[vec + r];
+      dl[r] = p.delta[vec + r];
+      named_bar(1, 128);
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      if (it > 0) mbar_wait(pds_free, (it - 1) & 1);
+      const bool diag = p.causal && qi == kj;
+#pragma unroll 1
+      for (int c0 = 0; c0 < T128; c0 += 32) {
+        float s[32], dp[32];
+        tmem_ld32(tmem + lb + kColS + c0, s);
+        tmem_ld32(tmem + lb + kColDP + c0, dp);
+        float pv[32], ds[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int c = c0 + i;
+          const float pr = (diag && c < r) ? 0.f : ex2f(s[i] * p.scale_log2 - lse[c]);
+          pv[i] = pr;
+          ds[i] = pr * (dp[i] - dl[c]) * p.scale;
+        }
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint4 up, ud;
+          __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&up);
+          __nv_bfloat162* hd = reinterpret_cast<__nv_bfloat162*>(&ud);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            hp[i] = __floats2bfloat162_rn(pv[8 * g + 2 * i], pv[8 * g + 2 * i + 1]);
+            hd[i] = __floats2bfloat162_rn(ds[8 * g + 2 * i], ds[8 * g + 2 * i + 1]);
+          }
+          *reinterpret_cast<uint4*>(sP + swz(r, c0 / 8 + g)) = up;
+          *reinterpret_cast<uint4*>(sDS + swz(r, c0 / 8 + g)) = ud;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+    }
+    // dK, dV rows of this key tile -> dqkv.
+    mbar_wait(dkv_done, 0);
+    tc_fence_after();
+    const int64_t row = static_cast<int64_t>(b) * p.seq + kj * T128 + r;
+    __nv_bfloat16* out = p.dqkv + row * 3 * p.hidden + head * D;
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      const uint32_t col = part ? kColDV : Cfg::kColDK;
+      __nv_bfloat16* dst = out + (part ? 2 : 1) * p.hidden;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + lb + col + c, v);
+#pragma unroll
+        for (int g = 0; g < 32; g += 8) {
+          uint4 u;
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(v[g + 2 * i], v[g + 2 * i + 1]);
+          *reinterpret_cast<uint4*>(dst + c + g) = u;
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------ dQ drain (query rows)
+    const int ew = warp & 3;
+    const int r = ew * 32 + lane;
+    const uint32_t lb = static_cast<uint32_t>(ew * 32) << 16;
+    for (int it = 0; it < n_it; ++it) {
+      const int qi = i0 + it;
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      float* dst = p.dq_acc + (static_cast<int64_t>(b) * p.seq + qi * T128 + r) * p.hidden + head * D;
+#pragma unroll 1
+      for (int c = 0; c < D; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + lb + kColDP + c, v);
+#pragma unroll
+        for (int g = 0; g < 32; g += 4) red_add_v4(dst + c + g, v[g], v[g + 1], v[g + 2], v[g + 3]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_free);
+    }
+  }
+
+  tc_fence_before();
+  __syncwarp();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// Delta[b, h, q] = sum_d dO * O over the head's D columns; warp per (row, head).
+__global__ void attn_bwd_prep_k(const __nv_bfloat16* dout, const __nv_bfloat16* out, float* delta, int T, int heads,
+                                int D, int seq, int hidden) {
+  const int wid = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (wid >= T * heads) return;
+  const int t = wid / heads, hd = wid % heads;
+  const __nv_bfloat16* a = dout + static_cast<int64_t>(t) * hidden + hd * D;
+  const __nv_bfloat16* o = out + static_cast<int64_t>(t) * hidden + hd * D;
+  float s = 0.f;
+  for (int c = lane * 2; c < D; c += 64) {
+    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + c));
+    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + c));
+    s += x.x * y.x + x.y * y.y;
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) {
+    const int b = t / seq, q = t % seq;
+    delta[(static_cast<int64_t>(b) * heads + hd) * seq + q] = s;
+  }
+}
+
+// dqkv[:, 0:h] = bf16(dq_acc)
+__global__ void dq_finish_k(const float* dq, __nv_bfloat16* dqkv, int T, int hidden) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (i >= static_cast<int64_t>(T) * hidden) return;
+  const int64_t t = i / hidden, c = i % hidden;
+  const float4 v = *reinterpret_cast<const float4*>(dq + i);
+  __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(dqkv + t * 3 * hidden + c);
+  d[0] = __floats2bfloat162_rn(v.x, v.y);
+  d[1] = __floats2bfloat162_rn(v.z, v.w);
+}
+
+CUtensorMap bw_map(const void* base, const AttnShape& s, int64_t ld_elems) {
+  CUtensorMap m;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(s.head_dim), static_cast<cuuint64_t>(s.heads),
+                        static_cast<cuuint64_t>(s.seq), static_cast<cuuint64_t>(s.mbs)};
+  const uint64_t ld = ld_elems * 2;
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(s.head_dim) * 2, ld, ld * s.seq};
+  cuuint32_t box[4] = {64, 1, 128, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = get_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("attention tensor map: " + std::to_string(int(r)));
+  return m;
+}
+
+template <int D>
+void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const float* lse2, const float* delta,
+                float* dq_acc, void* dqkv, cudaStream_t stream) {
+  auto* k = flash_bwd_kernel<D>;
+  static uint64_t attr_done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_done >> (dev & 63) & 1)) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, BwCfg<D>::SMEM);
+    attr_done |= 1ull << (dev & 63);
+  }
+  const auto* base = static_cast<const __nv_bfloat16*>(qkv);
+  const int64_t ld = 3LL * s.hidden;
+  const CUtensorMap mq = bw_map(base, s, ld), mk = bw_map(base + s.hidden, s, ld),
+                    mv = bw_map(base + 2 * s.hidden, s, ld), mdo = bw_map(dout, s, s.hidden);
+  BwParams p;
+  p.seq = s.seq;
+  p.heads = s.heads;
+  p.n_tiles = s.seq / T128;
+  p.causal = s.causal;
+  p.hidden = s.hidden;
+  p.scale = 1.f / sqrtf(static_cast<float>(D));
+  p.scale_log2 = 1.4426950408889634f * p.scale;
+  p.lse2 = lse2;
+  p.delta = delta;
+  p.dq_acc = dq_acc;
+  p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
+  const int grid = p.n_tiles * s.heads * s.mbs;
+  k<<<grid, BW_THREADS, BwCfg<D>::SMEM, stream>>>(mq, mk, mv, mdo, p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("flash_attn_bwd: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const void* dout, const float* lse2,
+                   float* delta, float* dq_acc, void* dqkv, cudaStream_t stream) {
+  if (s.seq % 128 || (s.head_dim != 64 && s.head_dim != 128)) {
+    throw std::runtime_error("flash_attn_bwd: needs seq % 128 == 0 and head_dim in {64, 128}");
+  }
+  const int T = s.mbs * s.seq;
+  const int warps = T * s.heads;
+  attn_bwd_prep_k<<<(warps + 7) / 8, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(dout),
+                                                       static_cast<const __nv_bfloat16*>(out), delta, T, s.heads,
+                                                       s.head_dim, s.seq, s.hidden);
+  cudaMemsetAsync(dq_acc, 0, sizeof(float) * T * s.hidden, stream);
+  if (s.head_dim == 128) launch_bwd<128>(s, qkv, dout, lse2, delta, dq_acc, dqkv, stream);
+  else launch_bwd<64>(s, qkv, dout, lse2, delta, dq_acc, dqkv, stream);
+  const int64_t n4 = static_cast<int64_t>(T) * s.hidden / 4;
+  dq_finish_k<<<static_cast<int>((n4 + 255) / 256), 256, 0, stream>>>(dq_acc, static_cast<__nv_bfloat16*>(dqkv), T,
+                                                                      s.hidden);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("flash_attn_bwd: ") + cudaGetErrorString(e));
+  return 3;
+}
+
+}  // namespace wpk

@@ -11,6 +11,7 @@
 #include <stdexcept>
 
 #include "capi_internal.hpp"
+#include "kernels/attention.cuh"
 #include "runtime/nccl_shim.hpp"
 #include "runtime/runtime.hpp"
 
@@ -114,7 +115,9 @@ struct DeviceState {
   void* shadow = nullptr;  // bf16 copy of master (bf16 mode)
   float* loss = nullptr;
   int32_t *tokens = nullptr, *labels = nullptr;
-  float* scores = nullptr;  // fp32 [mbs, heads, seq, seq] scratch
+  float* scores = nullptr;  // fp32 [mbs, heads, seq, seq] scratch (unfused attention)
+  float* attn_delta = nullptr;  // fp32 [mbs, heads, seq] (fused attention backward)
+  float* dq_acc = nullptr;      // fp32 [T, h]             (fused attention backward)
   std::vector<std::pair<int, int>> be_partner;  // per position: (device, position) of a BE's counterpart
 
   // per-step program state
@@ -254,7 +257,8 @@ Runtime::~Runtime() {
     if (d->step_begin) cudaEventDestroy(d->step_begin);
     for (void* p : {static_cast<void*>(d->master), static_cast<void*>(d->grad), static_cast<void*>(d->m),
                     static_cast<void*>(d->v), d->shadow, static_cast<void*>(d->loss), static_cast<void*>(d->tokens),
-                    static_cast<void*>(d->labels), static_cast<void*>(d->scores)})
+                    static_cast<void*>(d->labels), static_cast<void*>(d->scores),
+                    static_cast<void*>(d->attn_delta), static_cast<void*>(d->dq_acc)})
       if (p) cudaFree(p);
     d->pool.reset();
     if (d->compute) cudaStreamDestroy(d->compute);
@@ -328,8 +332,13 @@ void Runtime::build_devices(const int* device_ids) {
     ck(cudaMalloc(&d->loss, sizeof(float)), "cudaMalloc loss");
     ck(cudaMalloc(&d->tokens, sizeof(int32_t) * B * T), "cudaMalloc tokens");
     ck(cudaMalloc(&d->labels, sizeof(int32_t) * B * T), "cudaMalloc labels");
-    const size_t sc = sizeof(float) * size_t(m_.mbs) * m_.heads * m_.seq * m_.seq;
-    ck(cudaMalloc(&d->scores, sc), "cudaMalloc scores");
+    if (use_flash()) {
+      ck(cudaMalloc(&d->attn_delta, sizeof(float) * size_t(m_.mbs) * m_.heads * m_.seq), "cudaMalloc delta");
+      ck(cudaMalloc(&d->dq_acc, sizeof(float) * size_t(T) * m_.hidden), "cudaMalloc dq");
+    } else {
+      const size_t sc = sizeof(float) * size_t(m_.mbs) * m_.heads * m_.seq * m_.seq;
+      ck(cudaMalloc(&d->scores, sc), "cudaMalloc scores");
+    }
     init_params(*d);
     ck(cudaDeviceSynchronize(), "init sync");
     devs_.push_back(std::move(d));
@@ -638,6 +647,15 @@ void Runtime::gemm(DeviceState& d, const wpk::GemmProblem& g) {
   d.gemm_recs.push_back({2.0 * g.M * g.N * g.K * g.nb1 * g.nb2, s, e, shape});
 }
 
+bool Runtime::use_flash() const {
+  static const bool off = std::getenv("WP_NO_FLASH") != nullptr;
+  return !off && m_.dtype == wpk::kBF16 && wpk::flash_supported(attn_shape());
+}
+
+wpk::AttnShape Runtime::attn_shape() const {
+  return wpk::AttnShape{m_.mbs, m_.seq, m_.heads, m_.head_dim(), m_.hidden, m_.causal ? 1 : 0};
+}
+
 cudaEvent_t Runtime::next_event(DeviceState& d) {
   if (d.ev_next == d.events.size()) {
     DevGuard g(d.cuda);
@@ -695,29 +713,36 @@ BufPtr Runtime::unit_fwd(DeviceState& d, int ui, int mb, BufPtr x, UnitStash& st
     g.B = op(weight(d, L + "attn.qkv.w"), h, false);
     g.epi.c = st.a->p, g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.bias = master(d, L + "attn.qkv.b");
     gemm(d, g);
-    // S = Q K^T / sqrt(d), per (head, sequence)
-    wpk::GemmProblem sg;
-    sg.in_dtype = dt;
-    sg.M = S, sg.N = S, sg.K = dh, sg.nb1 = H, sg.nb2 = m_.mbs;
-    sg.causal = m_.causal ? wpk::kCausalSkipUpper : wpk::kCausalNone;
-    sg.A = op(st.a->p, 3 * h, false, dh, int64_t(S) * 3 * h);
-    sg.B = op(at(st.a, h, es), 3 * h, false, dh, int64_t(S) * 3 * h);
-    sg.epi.c = d.scores, sg.epi.c_dtype = wpk::kF32, sg.epi.ldc = S, sg.epi.c_b1 = int64_t(S) * S,
-    sg.epi.c_b2 = int64_t(H) * S * S, sg.epi.alpha = 1.0f / std::sqrt(static_cast<float>(dh));
-    gemm(d, sg);
-    st.b = act(int64_t(m_.mbs) * H * S * S);  // P
-    launches_ += wpk::softmax_fwd(dt, d.scores, st.b->p, m_.mbs * H * S, S, m_.causal, cs);
-    if (check_ops_enabled()) check_softmax(dt, d.scores, st.b->p, m_.mbs * H * S, S, m_.causal, cs);
-    // ctx = P V
-    st.c = act(int64_t(T) * h);
-    wpk::GemmProblem pv;
-    pv.in_dtype = dt;
-    pv.M = S, pv.N = dh, pv.K = S, pv.nb1 = H, pv.nb2 = m_.mbs;
-    pv.causal = m_.causal ? wpk::kCausalKUpToRow : wpk::kCausalNone;
-    pv.A = op(st.b->p, S, false, int64_t(S) * S, int64_t(H) * S * S);
-    pv.B = op(at(st.a, 2 * h, es), 3 * h, true, dh, int64_t(S) * 3 * h);
-    pv.epi.c = st.c->p, pv.epi.c_dtype = dt, pv.epi.ldc = h, pv.epi.c_b1 = dh, pv.epi.c_b2 = int64_t(S) * h;
-    gemm(d, pv);
+    if (use_flash()) {
+      // Fused attention: ctx and the per-row log-sum-exp (the stash replaces P).
+      st.b = f32(int64_t(m_.mbs) * H * S);
+      st.c = act(int64_t(T) * h);
+      launches_ += wpk::flash_attn_fwd(attn_shape(), st.a->p, st.c->p, static_cast<float*>(st.b->p), cs);
+    } else {
+      // S = Q K^T / sqrt(d), per (head, sequence)
+      wpk::GemmProblem sg;
+      sg.in_dtype = dt;
+      sg.M = S, sg.N = S, sg.K = dh, sg.nb1 = H, sg.nb2 = m_.mbs;
+      sg.causal = m_.causal ? wpk::kCausalSkipUpper : wpk::kCausalNone;
+      sg.A = op(st.a->p, 3 * h, false, dh, int64_t(S) * 3 * h);
+      sg.B = op(at(st.a, h, es), 3 * h, false, dh, int64_t(S) * 3 * h);
+      sg.epi.c = d.scores, sg.epi.c_dtype = wpk::kF32, sg.epi.ldc = S, sg.epi.c_b1 = int64_t(S) * S,
+      sg.epi.c_b2 = int64_t(H) * S * S, sg.epi.alpha = 1.0f / std::sqrt(static_cast<float>(dh));
+      gemm(d, sg);
+      st.b = act(int64_t(m_.mbs) * H * S * S);  // P
+      launches_ += wpk::softmax_fwd(dt, d.scores, st.b->p, m_.mbs * H * S, S, m_.causal, cs);
+      if (check_ops_enabled()) check_softmax(dt, d.scores, st.b->p, m_.mbs * H * S, S, m_.causal, cs);
+      // ctx = P V
+      st.c = act(int64_t(T) * h);
+      wpk::GemmProblem pv;
+      pv.in_dtype = dt;
+      pv.M = S, pv.N = dh, pv.K = S, pv.nb1 = H, pv.nb2 = m_.mbs;
+      pv.causal = m_.causal ? wpk::kCausalKUpToRow : wpk::kCausalNone;
+      pv.A = op(st.b->p, S, false, int64_t(S) * S, int64_t(H) * S * S);
+      pv.B = op(at(st.a, 2 * h, es), 3 * h, true, dh, int64_t(S) * 3 * h);
+      pv.epi.c = st.c->p, pv.epi.c_dtype = dt, pv.epi.ldc = h, pv.epi.c_b1 = dh, pv.epi.c_b2 = int64_t(S) * h;
+      gemm(d, pv);
+    }
     BufPtr out = act(int64_t(T) * h);
     wpk::GemmProblem pr;
     pr.in_dtype = dt;
@@ -847,56 +872,63 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   dgrad(dy->p, h, h, weight(d, L + "attn.proj.w"), h, dctx->p);
   wgrad(dy->p, h, st.c->p, h, grad(d, L + "attn.proj.w"));
   launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "attn.proj.b"), T, h, h, cs);
-  // dP = dctx V^T  (fp32 scratch)
-  {
-    wpk::GemmProblem g;
-    g.in_dtype = dt;
-    g.M = S, g.N = S, g.K = dh, g.nb1 = H, g.nb2 = m_.mbs;
-    g.causal = m_.causal ? wpk::kCausalSkipUpper : wpk::kCausalNone;
-    g.A = op(dctx->p, h, false, dh, int64_t(S) * h);
-    g.B = op(at(st.a, 2 * h, es), 3 * h, false, dh, int64_t(S) * 3 * h);
-    g.epi.c = d.scores, g.epi.c_dtype = wpk::kF32, g.epi.ldc = S, g.epi.c_b1 = int64_t(S) * S,
-    g.epi.c_b2 = int64_t(H) * S * S;
-    gemm(d, g);
-  }
-  BufPtr dqkv = act(int64_t(T) * 3 * h);
-  // dV = P^T dctx
-  {
-    wpk::GemmProblem g;
-    g.in_dtype = dt;
-    g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
-    g.causal = m_.causal ? wpk::kCausalKFromRow : wpk::kCausalNone;
-    g.A = op(st.b->p, S, true, int64_t(S) * S, int64_t(H) * S * S);
-    g.B = op(dctx->p, h, true, dh, int64_t(S) * h);
-    g.epi.c = at(dqkv, 2 * h, es), g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh,
-    g.epi.c_b2 = int64_t(S) * 3 * h;
-    gemm(d, g);
-  }
-  // dS = P * (dP - rowsum(dP * P)) / sqrt(d), in place over P
-  launches_ += wpk::softmax_bwd(dt, d.scores, st.b->p, m_.mbs * H * S, S, 1.0f / std::sqrt(static_cast<float>(dh)),
-                                m_.causal, cs);
-  // dQ = dS K
-  {
-    wpk::GemmProblem g;
-    g.in_dtype = dt;
-    g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
-    g.causal = m_.causal ? wpk::kCausalKUpToRow : wpk::kCausalNone;
-    g.A = op(st.b->p, S, false, int64_t(S) * S, int64_t(H) * S * S);
-    g.B = op(at(st.a, h, es), 3 * h, true, dh, int64_t(S) * 3 * h);
-    g.epi.c = dqkv->p, g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh, g.epi.c_b2 = int64_t(S) * 3 * h;
-    gemm(d, g);
-  }
-  // dK = dS^T Q
-  {
-    wpk::GemmProblem g;
-    g.in_dtype = dt;
-    g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
-    g.causal = m_.causal ? wpk::kCausalKFromRow : wpk::kCausalNone;
-    g.A = op(st.b->p, S, true, int64_t(S) * S, int64_t(H) * S * S);
-    g.B = op(st.a->p, 3 * h, true, dh, int64_t(S) * 3 * h);
-    g.epi.c = at(dqkv, h, es), g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh,
-    g.epi.c_b2 = int64_t(S) * 3 * h;
-    gemm(d, g);
+  BufPtr dqkv;
+  if (use_flash()) {
+    dqkv = act(int64_t(T) * 3 * h);
+    launches_ += wpk::flash_attn_bwd(attn_shape(), st.a->p, st.c->p, dctx->p, static_cast<float*>(st.b->p),
+                                     d.attn_delta, d.dq_acc, dqkv->p, cs);
+  } else {
+    // dP = dctx V^T  (fp32 scratch)
+    {
+      wpk::GemmProblem g;
+      g.in_dtype = dt;
+      g.M = S, g.N = S, g.K = dh, g.nb1 = H, g.nb2 = m_.mbs;
+      g.causal = m_.causal ? wpk::kCausalSkipUpper : wpk::kCausalNone;
+      g.A = op(dctx->p, h, false, dh, int64_t(S) * h);
+      g.B = op(at(st.a, 2 * h, es), 3 * h, false, dh, int64_t(S) * 3 * h);
+      g.epi.c = d.scores, g.epi.c_dtype = wpk::kF32, g.epi.ldc = S, g.epi.c_b1 = int64_t(S) * S,
+      g.epi.c_b2 = int64_t(H) * S * S;
+      gemm(d, g);
+    }
+    dqkv = act(int64_t(T) * 3 * h);
+    // dV = P^T dctx
+    {
+      wpk::GemmProblem g;
+      g.in_dtype = dt;
+      g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
+      g.causal = m_.causal ? wpk::kCausalKFromRow : wpk::kCausalNone;
+      g.A = op(st.b->p, S, true, int64_t(S) * S, int64_t(H) * S * S);
+      g.B = op(dctx->p, h, true, dh, int64_t(S) * h);
+      g.epi.c = at(dqkv, 2 * h, es), g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh,
+      g.epi.c_b2 = int64_t(S) * 3 * h;
+      gemm(d, g);
+    }
+    // dS = P * (dP - rowsum(dP * P)) / sqrt(d), in place over P
+    launches_ += wpk::softmax_bwd(dt, d.scores, st.b->p, m_.mbs * H * S, S, 1.0f / std::sqrt(static_cast<float>(dh)),
+                                  m_.causal, cs);
+    // dQ = dS K
+    {
+      wpk::GemmProblem g;
+      g.in_dtype = dt;
+      g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
+      g.causal = m_.causal ? wpk::kCausalKUpToRow : wpk::kCausalNone;
+      g.A = op(st.b->p, S, false, int64_t(S) * S, int64_t(H) * S * S);
+      g.B = op(at(st.a, h, es), 3 * h, true, dh, int64_t(S) * 3 * h);
+      g.epi.c = dqkv->p, g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh, g.epi.c_b2 = int64_t(S) * 3 * h;
+      gemm(d, g);
+    }
+    // dK = dS^T Q
+    {
+      wpk::GemmProblem g;
+      g.in_dtype = dt;
+      g.M = S, g.N = dh, g.K = S, g.nb1 = H, g.nb2 = m_.mbs;
+      g.causal = m_.causal ? wpk::kCausalKFromRow : wpk::kCausalNone;
+      g.A = op(st.b->p, S, true, int64_t(S) * S, int64_t(H) * S * S);
+      g.B = op(st.a->p, 3 * h, true, dh, int64_t(S) * 3 * h);
+      g.epi.c = at(dqkv, h, es), g.epi.c_dtype = dt, g.epi.ldc = 3 * h, g.epi.c_b1 = dh,
+      g.epi.c_b2 = int64_t(S) * 3 * h;
+      gemm(d, g);
+    }
   }
   wgrad(dqkv->p, 3 * h, st.ln->p, h, grad(d, L + "attn.qkv.w"));
   launches_ += wpk::colsum_accum(dt, dqkv->p, grad(d, L + "attn.qkv.b"), T, 3 * h, 3 * h, cs);

@@ -27,6 +27,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "kernels/attention.cuh"
 #include "kernels/gemm.cuh"
 #include "kernels/ops.cuh"
 #include "runtime/model.hpp"
@@ -149,6 +150,8 @@ class Runtime {
   BufPtr unit_fwd(DeviceState& d, int unit, int mb, BufPtr x, UnitStash& st);
   BufPtr unit_bwd(DeviceState& d, int unit, int mb, UnitStash& st, BufPtr dy);
   void gemm(DeviceState& d, const wpk::GemmProblem& g);
+  bool use_flash() const;  // fused tcgen05 attention (bf16, seq % 128 == 0, head_dim 64/128)
+  wpk::AttnShape attn_shape() const;
   const void* weight(DeviceState& d, const std::string& name) const;  // act dtype (shadow or master)
   float* master(DeviceState& d, const std::string& name) const;
   float* grad(DeviceState& d, const std::string& name) const;
