@@ -16,8 +16,14 @@ host memory every step and the loss read back.  The per-step working set
 (~35 GB of weights, optimizer state and activations) is far larger than the
 126 MB L2, so no explicit flush is needed between steps.
 
-Multi-GPU (torchrun, one rank per GPU): NCCL transport, rank r = pipeline
-device r; fixed global batch (strong scaling); time = max over ranks.
+Multi-GPU (torchrun, one rank per GPU): rank r = pipeline device r; the
+inter-stage transport is the CUDA-IPC one (copy-engine pushes over NVLink
+into IPC-mapped landing slots, stream-memory-op flags; WP_TRANSPORT=nccl
+selects NCCL send/recv instead); fixed global batch (strong scaling); time =
+max over ranks.  The measured bubble merges every rank's trace (each
+relative to its own step start, taken right after a barrier).
+WP_BENCH_SHARE_GPU=1 maps every rank to cuda:0 (functional testing of the
+multi-process path on a 1-GPU box; not a measurement).
 """
 import argparse
 import json
@@ -216,20 +222,27 @@ def main():
     import paper_2308_15762_b200 as wp
     from paper_2308_15762_b200.data import synthetic_batch
 
-    torch.cuda.set_device(local_rank)
+    share = os.environ.get("WP_BENCH_SHARE_GPU") == "1"
+    dev = 0 if share else local_rank
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     args.gpus = world
     desc = model_desc(args)
     cfg = wp.make_config(wp.Scheme.Hanayo, world, args.microbatches, args.waves)
     sched = wp.generate_schedule(cfg)
-    if world > 1:
+    transport = os.environ.get("WP_TRANSPORT", "ipc")
+    if world > 1 and transport == "nccl":
         obj = [wp.runtime.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_NCCL, device_ids=[local_rank], rank=rank,
-                        nccl_id=obj[0])
+        rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_NCCL, device_ids=[dev], rank=rank, nccl_id=obj[0])
+    elif world > 1:
+        rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_IPC, device_ids=[dev], rank=rank)
     else:
-        rt = wp.Runtime(desc, sched, device_ids=[local_rank])
+        rt = wp.Runtime(desc, sched, device_ids=[dev])
 
     tok_np, lab_np = synthetic_batch(args.microbatches, args.mbs, desc.seq, desc.vocab)
     tok_d = torch.from_numpy(tok_np).cuda()
@@ -254,9 +267,12 @@ def main():
         barrier()
         sec = st.elapsed_time(en) / 1e3
         if world > 1:
-            t = torch.tensor([sec], device="cuda")
+            t = torch.tensor([sec], device="cpu" if share else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             sec = float(t.item())
+            lt = torch.tensor([loss], device="cpu" if share else "cuda")
+            dist.all_reduce(lt)  # the loss lives on the rank holding the head slice
+            loss = float(lt.item())
         return sec, loss
 
     for _ in range(args.warmup):
@@ -265,7 +281,7 @@ def main():
     # Device-resident timed region (value), with GEMM profiling and clocks.
     rt.set_profiling(True)
     launches0 = rt.launch_count()
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(dev)
     clocks.start()
     sec, loss = timed(args.steps, host=False)
     clk = clocks.stop()
@@ -278,12 +294,26 @@ def main():
     # End-to-end through the public API from pinned host buffers.
     sec_e2e, _ = timed(args.steps, host=True)
 
-    # One traced step: measured vs simulated bubble.
+    # One traced step: measured vs simulated bubble.  Each rank traces its
+    # own pipeline device relative to its step start (right after a
+    # barrier); rank 0 merges them into one trace (wp_trace_build).
     rt.set_tracing(True)
+    barrier()
     rt.train_step(tok_d, lab_d)
     rt.set_tracing(False)
     tr = rt.trace()
+    if world > 1:
+        mine = (tr.intervals[rank], [e for e in tr.comm_events if e.src_device == rank])
+        parts = [None] * world
+        dist.all_gather_object(parts, mine)
+        tr = wp.build_trace([p[0] for p in parts], [e for p in parts for e in p[1]])
     measured_bubble = wp.bubble_ratio(tr)
+    msg_bytes = desc.tokens_per_microbatch * desc.hidden * 2
+    copies = [e.arrival_time - e.post_time for e in tr.comm_events if e.arrival_time > e.post_time]
+    p2p = {"messages": len(tr.comm_events), "bytes_per_message": msg_bytes,
+           "mean_copy_us": 1e6 * statistics.mean(copies) if copies else None,
+           "mean_copy_gbs": msg_bytes / statistics.mean(copies) / 1e9 if copies else None,
+           "transport": transport if world > 1 else "none (P=1)"}
     fwd = [iv.end - iv.start for dev in tr.intervals for iv in dev if iv.kind == wp.ActionKind.Forward]
     bwd = [iv.end - iv.start for dev in tr.intervals for iv in dev if iv.kind == wp.ActionKind.Backward]
     tf, tb = statistics.mean(fwd) * 2 * args.waves, statistics.mean(bwd) * 2 * args.waves
@@ -292,6 +322,9 @@ def main():
     eq1 = wp.analytic_bubble_hanayo_d(world, args.waves, tf, tb, 0.0) if world >= 2 else None
 
     if rank != 0:
+        dist.barrier()  # peers' IPC mappings stay valid until every rank is done
+        rt.close()
+        dist.destroy_process_group()
         return
     samples = args.microbatches * args.mbs * args.steps
     value = samples / sec
@@ -320,6 +353,7 @@ def main():
         "tc_peak_frac": flops_step * args.steps / sec / world / (peak_tc * 1e12),
         "bubble": {"measured": measured_bubble, "simulated_at_measured_costs": sim_bubble, "eq1": eq1,
                    "t_forward_s": tf, "t_backward_s": tb},
+        "p2p": p2p,
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05, all GEMM launches of the step)",
                      "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
                      "frac": achieved / peak_tc if achieved else None, "traffic": traffic,
@@ -333,6 +367,8 @@ def main():
         "loss": loss,
     }
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
     rt.close()
     if world > 1:
         dist.destroy_process_group()

@@ -107,6 +107,13 @@ int wp_trace_devices(const wp_trace* trace, int* devices);
 int wp_trace_intervals(const wp_trace* trace, int device, const wp_interval** iv, int* count);
 int wp_trace_comm_events(const wp_trace* trace, const wp_comm_event** ev, int* count);
 void wp_trace_free(wp_trace* trace);
+/* A trace assembled by the caller -- e.g. the measured traces of the ranks
+ * of a multi-process job gathered into one -- so bubble_ratio and
+ * memory_profile apply unchanged: `counts[d]` intervals of device d,
+ * concatenated device-major, plus `n_events` comm events.  The makespan is
+ * the latest interval end or arrival (src/simulate.cpp:166-169). */
+int wp_trace_build(int devices, const int* counts, const wp_interval* intervals, int n_events,
+                   const wp_comm_event* events, wp_trace** out);
 
 /* bubble_ratio, src/analytics.cpp:32-46. */
 int wp_bubble_ratio(const wp_trace* trace, double* out);
@@ -149,13 +156,25 @@ typedef struct wp_runtime wp_runtime;
  *    device d runs on CUDA ordinal device_ids[d] (ids may repeat: several
  *    pipeline devices sharing one GPU, each with its own streams).
  *  WP_TRANSPORT_NCCL: one process per pipeline device (rank == device);
- *    `nccl_id` is the 128-byte ncclUniqueId broadcast by the caller. */
-enum { WP_TRANSPORT_LOCAL = 0, WP_TRANSPORT_NCCL = 1 };
+ *    `nccl_id` is the 128-byte ncclUniqueId broadcast by the caller.
+ *  WP_TRANSPORT_IPC: one process per pipeline device (rank == device);
+ *    messages are copy-engine pushes over NVLink into the receiver's
+ *    CUDA-IPC-mapped landing slots, signalled by stream memory operations
+ *    (no SMs spent on transfers).  After creation every rank exports
+ *    wp_runtime_ipc_handle, the caller all-gathers the handles (rank order)
+ *    and passes them to wp_runtime_ipc_connect before the first step.
+ *    `nccl_id` is ignored. */
+enum { WP_TRANSPORT_LOCAL = 0, WP_TRANSPORT_NCCL = 1, WP_TRANSPORT_IPC = 2 };
 
 int wp_runtime_create(const wp_model_desc* model, const wp_list* list, int transport,
                       const int* device_ids, int rank, const void* nccl_id,
                       wp_runtime** out);
 void wp_runtime_free(wp_runtime* rt);
+/* IPC transport handshake.  `out` receives WP_IPC_HANDLE_BYTES bytes;
+ * `handles` holds nranks of them, rank-major. */
+#define WP_IPC_HANDLE_BYTES 64
+int wp_runtime_ipc_handle(wp_runtime* rt, void* out);
+int wp_runtime_ipc_connect(wp_runtime* rt, const void* handles, int nranks);
 /* ncclGetUniqueId for rank 0 of a WP_TRANSPORT_NCCL job (128 bytes). */
 int wp_nccl_unique_id(void* out128);
 

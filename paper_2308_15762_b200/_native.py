@@ -83,6 +83,7 @@ _SIGS = {
     "wp_trace_intervals": (I, [P, I, C.POINTER(C.POINTER(wp_interval)), IP]),
     "wp_trace_comm_events": (I, [P, C.POINTER(C.POINTER(wp_comm_event)), IP]),
     "wp_trace_free": (None, [P]),
+    "wp_trace_build": (I, [I, IP, C.POINTER(wp_interval), I, C.POINTER(wp_comm_event), PP]),
     "wp_bubble_ratio": (I, [P, DP]),
     "wp_memory_profile": (I, [P, P, I64P, I64P]),
     "wp_analytic_bubble": (I, [I, I, D, D, D, DP]),
@@ -91,6 +92,8 @@ _SIGS = {
     "wp_runtime_create": (I, [C.POINTER(wp_model_desc), P, I, IP, I, C.c_void_p, PP]),
     "wp_runtime_free": (None, [P]),
     "wp_nccl_unique_id": (I, [C.c_void_p]),
+    "wp_runtime_ipc_handle": (I, [P, C.c_void_p]),
+    "wp_runtime_ipc_connect": (I, [P, C.c_void_p, I]),
     "wp_train_step": (I, [P, C.c_void_p, C.c_void_p, I, C.POINTER(C.c_float)]),
     "wp_runtime_trace": (I, [P, PP]),
     "wp_runtime_set_tracing": (I, [P, I]),

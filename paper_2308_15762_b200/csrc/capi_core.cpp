@@ -1,6 +1,7 @@
 // C ABI over the schedule path (include/wavepipe.h).  Every entry point
 // catches, maps the exception type to the reference CLI's exit-code taxonomy
 // (tools/main.cpp:37-40, :297-312) and stores the message for wp_last_error.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -293,6 +294,47 @@ int wp_trace_comm_events(const wp_trace* t, const wp_comm_event** ev, int* count
 }
 
 void wp_trace_free(wp_trace* t) { delete t; }
+
+int wp_trace_build(int devices, const int* counts, const wp_interval* iv, int n_events, const wp_comm_event* ev,
+                   wp_trace** out) {
+  try {
+    if (devices < 0 || n_events < 0 || !out || (devices > 0 && !counts) || (n_events > 0 && !ev)) {
+      return fail(WP_ERR_CONFIG, "null or negative argument");
+    }
+    auto* t = new wp_trace;
+    t->trace.intervals.resize(devices);
+    int64_t k = 0;
+    for (int d = 0; d < devices; ++d) {
+      if (counts[d] < 0) {
+        delete t;
+        return fail(WP_ERR_CONFIG, "negative interval count");
+      }
+      for (int i = 0; i < counts[d]; ++i, ++k) {
+        const wp_interval& x = iv[k];
+        wavepipe::TraceInterval y;
+        y.action_index = x.action_index;
+        y.kind = static_cast<wavepipe::ActionKind>(x.kind);
+        y.microbatch = x.microbatch;
+        y.slice_index = x.slice_index;
+        y.direction = static_cast<wavepipe::Direction>(x.direction);
+        y.start = x.start;
+        y.end = x.end;
+        t->trace.makespan = std::max(t->trace.makespan, y.end);
+        t->trace.intervals[d].push_back(y);
+      }
+    }
+    for (int i = 0; i < n_events; ++i) {
+      t->trace.comm_events.push_back(
+          wavepipe::CommEvent{ev[i].src_device, ev[i].dst_device, ev[i].post_time, ev[i].arrival_time});
+      t->trace.makespan = std::max(t->trace.makespan, ev[i].arrival_time);
+    }
+    refresh(t);
+    *out = t;
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
 
 int wp_bubble_ratio(const wp_trace* t, double* out) {
   try {

@@ -45,6 +45,26 @@ int wp_runtime_create(const wp_model_desc* model, const wp_list* list, int trans
 
 void wp_runtime_free(wp_runtime* rt) { delete rt; }
 
+int wp_runtime_ipc_handle(wp_runtime* rt, void* out) {
+  try {
+    if (!rt || !out) return fail(WP_ERR_CONFIG, "null argument");
+    rt->rt->ipc_handle(out);
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int wp_runtime_ipc_connect(wp_runtime* rt, const void* handles, int nranks) {
+  try {
+    if (!rt || !handles) return fail(WP_ERR_CONFIG, "null argument");
+    rt->rt->ipc_connect(handles, nranks);
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 int wp_nccl_unique_id(void* out128) {
   if (!out128) return fail(WP_ERR_CONFIG, "null argument");
   ncclUniqueId id;

@@ -1,0 +1,105 @@
+// Private state of the GPU runtime shared by its translation units
+// (executor.cpp: action interpreter and unit kernels; ipc.cpp: CUDA-IPC
+// transport).  Not part of the public interface.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "capi_internal.hpp"
+#include "runtime/nccl_shim.hpp"
+#include "runtime/runtime.hpp"
+
+namespace wprt {
+
+using wavepipe::ActionKind;
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw wpc::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+inline void ckn(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw wpc::CudaError(std::string(what) + ": " + NcclApi::get().GetErrorString(r));
+}
+
+// Message identity (payload, microbatch, lower slice of the boundary), the
+// reference's matching key (src/schedule.cpp:315-324, src/simulate.cpp:39-46).
+inline MsgKey message_key(const wavepipe::Action& a) {
+  const bool act = a.payload == static_cast<int>(wavepipe::Payload::Activation);
+  const bool out = a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange;
+  return MsgKey{a.payload, a.microbatch,
+                act ? (out ? a.slice_index : a.slice_index - 1) : (out ? a.slice_index - 1 : a.slice_index)};
+}
+
+struct DevGuard {
+  int prev = 0;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() { cudaSetDevice(prev); }
+};
+
+struct DeviceState {
+  int pipe = 0;  // pipeline device (index into the ActionList)
+  int cuda = 0;  // CUDA ordinal
+  cudaStream_t compute = nullptr, copy = nullptr;
+  std::unique_ptr<Pool> pool;
+  std::vector<ParamSlot> params;
+  std::unordered_map<std::string, int> by_name;
+  int64_t nparam = 0;
+  float *master = nullptr, *grad = nullptr, *m = nullptr, *v = nullptr;
+  void* shadow = nullptr;  // bf16 copy of master (bf16 mode)
+  float* loss = nullptr;
+  int32_t *tokens = nullptr, *labels = nullptr;
+  float* scores = nullptr;  // fp32 [mbs, heads, seq, seq] scratch (unfused attention)
+  float* attn_delta = nullptr;  // fp32 [mbs, heads, seq] (fused attention backward)
+  float* dq_acc = nullptr;      // fp32 [T, h]             (fused attention backward)
+  std::vector<std::pair<int, int>> be_partner;  // per position: (device, position) of a BE's counterpart
+
+  // per-step program state
+  size_t pc = 0;
+  std::map<std::pair<int, int>, SliceStash> stash;
+  std::map<MsgKey, BufPtr> handoff, inbox, outbox;
+  std::map<MsgKey, cudaEvent_t> outbox_ready;
+  std::vector<cudaEvent_t> pending;
+  cudaEvent_t last_start = nullptr;
+  cudaEvent_t step_begin = nullptr;
+  std::vector<cudaEvent_t> events;
+  size_t ev_next = 0;
+  std::vector<uint8_t> published_at;  // BE positions whose outgoing message is published
+  // NCCL transport: per-peer send / receive streams and the step's posted
+  // receives (landing buffer + arrival event per message).
+  std::map<int, cudaStream_t> tx, rx;
+  std::map<MsgKey, std::pair<BufPtr, cudaEvent_t>> posted;
+  // IPC transport: arrival flags (local memory) the next compute must see
+  // reach this step's epoch before it starts.
+  std::vector<uint32_t*> pending_flags;
+
+  struct Rec {
+    int idx;
+    ActionKind kind;
+    int mb, slice;
+    cudaEvent_t s, e;
+  };
+  struct CommRec {
+    int src, dst;
+    cudaEvent_t post, arrive;
+    DeviceState* post_dev;
+    DeviceState* arrive_dev;
+  };
+  std::vector<Rec> recs;
+  std::vector<CommRec> comm_recs;
+  struct GemmRec {
+    double flops;
+    cudaEvent_t s, e;
+    std::string shape;
+  };
+  std::vector<GemmRec> gemm_recs;
+};
+
+}  // namespace wprt

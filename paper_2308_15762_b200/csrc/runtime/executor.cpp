@@ -12,8 +12,10 @@
 
 #include "capi_internal.hpp"
 #include "kernels/attention.cuh"
+#include "runtime/device_state.hpp"
 #include "runtime/nccl_shim.hpp"
 #include "runtime/runtime.hpp"
+#include "runtime/stream_ops.hpp"
 
 namespace wprt {
 
@@ -22,31 +24,9 @@ using wavepipe::ActionKind;
 
 namespace {
 
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw wpc::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
-}
-void ckn(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) throw wpc::CudaError(std::string(what) + ": " + NcclApi::get().GetErrorString(r));
-}
-
-struct DevGuard {
-  int prev = 0;
-  explicit DevGuard(int d) {
-    cudaGetDevice(&prev);
-    if (prev != d) cudaSetDevice(d);
-  }
-  ~DevGuard() { cudaSetDevice(prev); }
-};
-
 constexpr int kAct = static_cast<int>(wavepipe::Payload::Activation);
 constexpr int kGrad = static_cast<int>(wavepipe::Payload::Gradient);
 
-MsgKey key_of(const Action& a) {
-  const bool act = a.payload == kAct;
-  const bool out = a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange;
-  return MsgKey{a.payload, a.microbatch,
-                act ? (out ? a.slice_index : a.slice_index - 1) : (out ? a.slice_index - 1 : a.slice_index)};
-}
 
 uint64_t name_hash(const std::string& s) {
   uint64_t h = 1469598103934665603ull;
@@ -89,6 +69,11 @@ BufPtr Pool::alloc(size_t bytes, cudaStream_t stream, int cls) {
 
 void Pool::release(const BufPtr& b, cudaStream_t stream) {
   if (!b) return;
+  if (b->pool_class == 2) {
+    // IPC landing slot: hand it back to its sender for the next step.
+    StreamOps::write(stream, b->ipc_free_remote, b->ipc_epoch);
+    return;
+  }
   // Message buffers and anything released off the compute stream carry an
   // event: the next owner (possibly another stream or device) waits on it.
   if (b->pool_class == 1 || stream != home_) {
@@ -102,61 +87,6 @@ void Pool::release(const BufPtr& b, cudaStream_t stream) {
   free_[{b->pool_class, b->bytes}].push_back(b);
 }
 
-// ------------------------------------------------------------- device state
-struct DeviceState {
-  int pipe = 0;  // pipeline device (index into the ActionList)
-  int cuda = 0;  // CUDA ordinal
-  cudaStream_t compute = nullptr, copy = nullptr;
-  std::unique_ptr<Pool> pool;
-  std::vector<ParamSlot> params;
-  std::unordered_map<std::string, int> by_name;
-  int64_t nparam = 0;
-  float *master = nullptr, *grad = nullptr, *m = nullptr, *v = nullptr;
-  void* shadow = nullptr;  // bf16 copy of master (bf16 mode)
-  float* loss = nullptr;
-  int32_t *tokens = nullptr, *labels = nullptr;
-  float* scores = nullptr;  // fp32 [mbs, heads, seq, seq] scratch (unfused attention)
-  float* attn_delta = nullptr;  // fp32 [mbs, heads, seq] (fused attention backward)
-  float* dq_acc = nullptr;      // fp32 [T, h]             (fused attention backward)
-  std::vector<std::pair<int, int>> be_partner;  // per position: (device, position) of a BE's counterpart
-
-  // per-step program state
-  size_t pc = 0;
-  std::map<std::pair<int, int>, SliceStash> stash;
-  std::map<MsgKey, BufPtr> handoff, inbox, outbox;
-  std::map<MsgKey, cudaEvent_t> outbox_ready;
-  std::vector<cudaEvent_t> pending;
-  cudaEvent_t last_start = nullptr;
-  cudaEvent_t step_begin = nullptr;
-  std::vector<cudaEvent_t> events;
-  size_t ev_next = 0;
-  std::vector<uint8_t> published_at;  // BE positions whose outgoing message is published
-  // NCCL transport: per-peer send / receive streams and the step's posted
-  // receives (landing buffer + arrival event per message).
-  std::map<int, cudaStream_t> tx, rx;
-  std::map<MsgKey, std::pair<BufPtr, cudaEvent_t>> posted;
-
-  struct Rec {
-    int idx;
-    ActionKind kind;
-    int mb, slice;
-    cudaEvent_t s, e;
-  };
-  struct CommRec {
-    int src, dst;
-    cudaEvent_t post, arrive;
-    DeviceState* post_dev;
-    DeviceState* arrive_dev;
-  };
-  std::vector<Rec> recs;
-  std::vector<CommRec> comm_recs;
-  struct GemmRec {
-    double flops;
-    cudaEvent_t s, e;
-    std::string shape;
-  };
-  std::vector<GemmRec> gemm_recs;
-};
 
 // ------------------------------------------------------------------ runtime
 Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, int transport, const int* device_ids,
@@ -173,8 +103,11 @@ Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, in
     throw wavepipe::ConfigError(
         "tie_embeddings needs the first and last slice on one device (true for Hanayo placements)");
   }
-  if (transport_ != WP_TRANSPORT_LOCAL && transport_ != WP_TRANSPORT_NCCL) {
+  if (transport_ != WP_TRANSPORT_LOCAL && transport_ != WP_TRANSPORT_NCCL && transport_ != WP_TRANSPORT_IPC) {
     throw wavepipe::ConfigError("unknown transport");
+  }
+  if (transport_ == WP_TRANSPORT_IPC && (rank_ < 0 || rank_ >= P)) {
+    throw wavepipe::ConfigError("IPC transport needs 0 <= rank < P");
   }
   if (transport_ == WP_TRANSPORT_NCCL && (rank_ < 0 || rank_ >= P || !nccl_id)) {
     throw wavepipe::ConfigError("NCCL transport needs 0 <= rank < P and an ncclUniqueId");
@@ -189,6 +122,7 @@ Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, in
     nccl_comm_ = comm;
     build_channels();
   }
+  if (transport_ == WP_TRANSPORT_IPC) ipc_setup();
 }
 
 void Runtime::build_channels() {
@@ -198,7 +132,7 @@ void Runtime::build_channels() {
   std::map<std::pair<int, int>, std::vector<MsgKey>> plan;
   for (int p = 0; p < list_.config.devices; ++p)
     for (const Action& a : list_.per_device[p])
-      if (a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange) plan[{p, a.peer}].push_back(key_of(a));
+      if (a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange) plan[{p, a.peer}].push_back(message_key(a));
   DeviceState& d = *devs_[0];
   DevGuard g(d.cuda);
   for (auto& [pair, keys] : plan) {
@@ -247,6 +181,7 @@ void Runtime::post_channel_receives(DeviceState& d) {
 }
 
 Runtime::~Runtime() {
+  ipc_release();
   for (auto& c : channels_)
     if (c.comm) NcclApi::get().CommDestroy(static_cast<ncclComm_t>(c.comm));
   if (nccl_comm_) NcclApi::get().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
@@ -1025,6 +960,8 @@ bool Runtime::advance(DeviceState& d) {
     if (a.is_compute()) {
       for (cudaEvent_t e : d.pending) ck(cudaStreamWaitEvent(d.compute, e, 0), "wait arrival");
       d.pending.clear();
+      for (uint32_t* f : d.pending_flags) StreamOps::wait_geq(d.compute, f, epoch_);
+      d.pending_flags.clear();
       d.last_start = next_event(d);
       ck(cudaEventRecord(d.last_start, d.compute), "record start");
       if (a.kind == ActionKind::Forward) forward(d, a);
@@ -1036,6 +973,16 @@ bool Runtime::advance(DeviceState& d) {
       }
     } else if (a.kind == ActionKind::OptimizerStep) {
       optimizer(d);
+    } else if (transport_ == WP_TRANSPORT_IPC) {
+      if (a.kind == ActionKind::Receive) {
+        ipc_expect(d, message_key(a));
+      } else {
+        ipc_send(d, a);
+        if (a.kind == ActionKind::BatchedExchange) {
+          const auto [q, qi] = d.be_partner[d.pc];
+          ipc_expect(d, message_key(list_.per_device[q][qi]));
+        }
+      }
     } else if (transport_ == WP_TRANSPORT_NCCL) {
       // Receives were posted at step start (post_channel_receives); here a
       // Receive / the incoming half of an exchange only gates the next
@@ -1049,9 +996,9 @@ bool Runtime::advance(DeviceState& d) {
         d.posted.erase(it);
       };
       if (a.kind == ActionKind::Receive) {
-        arrive(key_of(a));
+        arrive(message_key(a));
       } else {
-        const MsgKey out = key_of(a);
+        const MsgKey out = message_key(a);
         auto it = d.outbox.find(out);
         if (it == d.outbox.end()) throw wavepipe::SimulationError("runtime: send before its producer");
         const Channel* ch = nullptr;
@@ -1067,7 +1014,7 @@ bool Runtime::advance(DeviceState& d) {
         d.outbox_ready.erase(out);
         if (a.kind == ActionKind::BatchedExchange) {
           const auto [q, qi] = d.be_partner[d.pc];
-          arrive(key_of(list_.per_device[q][qi]));
+          arrive(message_key(list_.per_device[q][qi]));
         }
       }
     } else {
@@ -1080,20 +1027,20 @@ bool Runtime::advance(DeviceState& d) {
         d.outbox_ready.erase(k);
       };
       if (a.kind == ActionKind::Send) {
-        publish(key_of(a));
+        publish(message_key(a));
       } else if (a.kind == ActionKind::Receive) {
-        auto it = published_.find(key_of(a));
+        auto it = published_.find(message_key(a));
         if (it == published_.end()) break;  // sender has not produced it yet
         Published msg = it->second;
         published_.erase(it);
-        post_copy(d, key_of(a), msg);
+        post_copy(d, message_key(a), msg);
       } else {  // BatchedExchange
         if (!d.published_at[d.pc]) {
-          publish(key_of(a));
+          publish(message_key(a));
           d.published_at[d.pc] = 1;
         }
         const auto [q, qi] = d.be_partner[d.pc];
-        const MsgKey kin = key_of(list_.per_device[q][qi]);
+        const MsgKey kin = message_key(list_.per_device[q][qi]);
         auto it = published_.find(kin);
         if (it == published_.end()) break;  // counterpart not at the exchange yet
         Published msg = it->second;
@@ -1126,6 +1073,10 @@ void Runtime::enqueue_step() {
 }
 
 float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_device) {
+  if (transport_ == WP_TRANSPORT_IPC && !ipc_connected_) {
+    throw wavepipe::ConfigError("IPC transport: call ipc_connect with every rank's handle before the first step");
+  }
+  epoch_ = static_cast<uint32_t>(step_ + 1);
   const size_t n = size_t(list_.config.microbatches) * m_.tokens();
   for (auto& d : devs_) {
     DevGuard g(d->cuda);
@@ -1139,6 +1090,7 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     d->pc = 0;
     d->ev_next = 0;
     d->pending.clear();
+    d->pending_flags.clear();
     d->last_start = nullptr;
     d->recs.clear();
     d->comm_recs.clear();

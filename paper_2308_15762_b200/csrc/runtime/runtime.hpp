@@ -41,9 +41,13 @@ namespace wprt {
 struct Buf {
   void* p = nullptr;
   size_t bytes = 0;
-  int pool_class = 0;  // 0 compute-only, 1 message
+  int pool_class = 0;  // 0 compute-only, 1 message, 2 IPC landing slot (not pool-owned)
   cudaEvent_t ev = nullptr;
   bool ev_pending = false;
+  // IPC landing slot: releasing it writes `ipc_epoch` into the sender's
+  // free flag (peer memory), letting the sender reuse the slot next step.
+  uint32_t* ipc_free_remote = nullptr;
+  uint32_t ipc_epoch = 0;
 };
 using BufPtr = std::shared_ptr<Buf>;
 
@@ -122,6 +126,12 @@ class Runtime {
 
   int param_count() const { return static_cast<int>(param_index_.size()); }
   const ParamDesc& param_desc(int i, bool* owned) const;
+  // IPC transport handshake: export this rank's landing arena (64-byte
+  // cudaIpcMemHandle_t), then map every peer's from the handles of all ranks.
+  void ipc_handle(void* out64) const;
+  void ipc_connect(const void* handles, int nranks);
+  // Bytes of one inter-stage message (activation or input-gradient).
+  size_t message_bytes() const { return size_t(m_.tokens()) * m_.hidden * m_.act_bytes(); }
   void get_param(const std::string& name, float* host, int64_t n, bool grad);
   void set_param(const std::string& name, const float* host, int64_t n);
 
@@ -189,6 +199,32 @@ class Runtime {
   std::vector<Channel> channels_;
   void build_channels();
   void post_channel_receives(DeviceState& d);
+
+  // CUDA-IPC transport (one process per GPU, copy-engine pushes over
+  // NVLink).  Every message of the list has a fixed landing slot in its
+  // receiver's arena and two 32-bit flags: arrive[m] in the receiver's arena
+  // (written by the sender's stream after the copy) and free[m] in the
+  // sender's arena (written by the receiver's stream when the slot is
+  // released).  Flags carry the step epoch, so nothing is reset between steps.
+  struct IpcMsg {
+    int src, dst;
+    size_t data_off;  // in the receiver's arena
+  };
+  std::map<MsgKey, int> ipc_index_;
+  std::vector<IpcMsg> ipc_msgs_;
+  char* ipc_arena_ = nullptr;
+  size_t ipc_flag_bytes_ = 0, ipc_arena_bytes_ = 0;
+  std::vector<char*> ipc_peer_;  // rank -> mapped arena (nullptr: not a neighbour)
+  bool ipc_connected_ = false;
+  uint32_t epoch_ = 0;
+  void ipc_setup();
+  void ipc_release();
+  uint32_t* ipc_arrive_flag(char* base, int m) const { return reinterpret_cast<uint32_t*>(base) + m; }
+  uint32_t* ipc_free_flag(char* base, int m) const {
+    return reinterpret_cast<uint32_t*>(base) + ipc_msgs_.size() + m;
+  }
+  void ipc_send(DeviceState& d, const wavepipe::Action& a);
+  void ipc_expect(DeviceState& d, const MsgKey& k);
 };
 
 }  // namespace wprt

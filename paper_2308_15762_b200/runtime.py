@@ -15,6 +15,8 @@ from .schedule import ActionList, SimTrace
 
 TRANSPORT_LOCAL = 0
 TRANSPORT_NCCL = 1
+TRANSPORT_IPC = 2
+IPC_HANDLE_BYTES = 64
 
 
 @dataclass
@@ -63,9 +65,27 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def _all_gather_bytes(blob: bytes):
+    """Default IPC handshake: all-gather over the initialised torch.distributed
+    group (rank order)."""
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        raise RuntimeError("TRANSPORT_IPC needs torch.distributed initialised or an `exchange` callable")
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, blob)
+    return out
+
+
 class Runtime:
+    """wp_runtime_create / wp_train_step.  transport:
+    TRANSPORT_LOCAL  all pipeline devices in this process (device_ids[d] per device);
+    TRANSPORT_NCCL   one process per pipeline device, NCCL send/recv (nccl_id);
+    TRANSPORT_IPC    one process per pipeline device, copy-engine pushes into
+                     CUDA-IPC-mapped landing slots; `exchange(bytes) -> [bytes]*P`
+                     all-gathers the handles (default: torch.distributed)."""
+
     def __init__(self, model: ModelDesc, schedule: ActionList, transport=TRANSPORT_LOCAL, device_ids=None,
-                 rank=0, nccl_id=None):
+                 rank=0, nccl_id=None, exchange=None):
         self.model = model
         self.schedule = schedule
         P = schedule.config.devices
@@ -81,6 +101,14 @@ class Runtime:
         check(lib.wp_runtime_create(C.byref(self._desc), schedule.handle, transport, self._ids, rank, nid,
                                     C.byref(h)))
         self._h = h
+        if transport == TRANSPORT_IPC:
+            mine = C.create_string_buffer(IPC_HANDLE_BYTES)
+            check(lib.wp_runtime_ipc_handle(self._h, mine))
+            blobs = (exchange or _all_gather_bytes)(mine.raw)
+            if len(blobs) != P or any(len(b) != IPC_HANDLE_BYTES for b in blobs):
+                raise ValueError("exchange must return one 64-byte handle per rank")
+            allh = C.create_string_buffer(b"".join(blobs), P * IPC_HANDLE_BYTES)
+            check(lib.wp_runtime_ipc_connect(self._h, allh, P))
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

@@ -19,7 +19,7 @@ from ._native import (ConfigError, ScheduleError, check, lib, wp_action, wp_comm
 
 __all__ = [
     "Scheme", "ActionKind", "Payload", "Direction", "ScheduleConfig", "CostModel", "Action",
-    "ActionList", "TraceInterval", "CommEvent", "SimTrace", "make_config", "generate_schedule",
+    "ActionList", "TraceInterval", "CommEvent", "SimTrace", "build_trace", "make_config", "generate_schedule",
     "insert_comm", "simulate", "bubble_ratio", "memory_profile", "activation_variance",
     "analytic_bubble_hanayo", "analytic_bubble_hanayo_d", "analytic_bubble_simplified",
     "serialize_action_list", "parse_action_list", "validate_all", "ConfigError", "ScheduleError",
@@ -235,6 +235,22 @@ class SimTrace:
         if getattr(self, "_owned", False) and self._h is not None and self._h.value:
             lib.wp_trace_free(self._h)
             self._h = None
+
+
+def build_trace(intervals, comm_events=()) -> SimTrace:
+    """wp_trace_build: a SimTrace from per-device interval lists (e.g. the
+    measured traces of all ranks of a multi-process job merged), so
+    bubble_ratio / memory_profile apply unchanged."""
+    counts = (C.c_int * max(len(intervals), 1))(*[len(d) for d in intervals])
+    flat = [iv for dev in intervals for iv in dev]
+    ivs = (wp_interval * max(len(flat), 1))(*[
+        wp_interval(i.action_index, int(i.kind), i.microbatch, i.slice_index, int(i.direction), i.start, i.end)
+        for i in flat])
+    evs = (wp_comm_event * max(len(comm_events), 1))(*[
+        wp_comm_event(e.src_device, e.dst_device, e.post_time, e.arrival_time) for e in comm_events])
+    h = C.c_void_p()
+    check(lib.wp_trace_build(len(intervals), counts, ivs, len(comm_events), evs, C.byref(h)))
+    return SimTrace(h)
 
 
 def simulate(lst: ActionList, cost: CostModel = None) -> SimTrace:
