@@ -91,3 +91,36 @@ extern "C" int wp_debug_flash_bwd(int mbs, int seq, int heads, int head_dim, int
     return wpc::map_exception();
   }
 }
+
+#include "kernels/ops.cuh"
+
+namespace {
+int sync_status(const char* what) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return wpc::fail(WP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return WP_OK;
+}
+}  // namespace
+
+extern "C" int wp_debug_layernorm(int dtype, int T, int h, const void* x, const float* w, const float* b, void* y,
+                                  float* mean, float* rstd, const void* dy, const void* dres, void* dx, float* dw,
+                                  float* db) {
+  try {
+    wpk::layernorm_fwd(dtype, x, w, b, y, mean, rstd, T, h, nullptr);
+    if (dy) wpk::layernorm_bwd(dtype, dy, x, mean, rstd, w, dres, dx, dw, db, T, h, nullptr);
+    return sync_status("layernorm");
+  } catch (...) {
+    return wpc::map_exception();
+  }
+}
+
+extern "C" int wp_debug_xent(int dtype, void* logits, const int32_t* labels, float* loss, int T, int V,
+                             float loss_scale, float grad_scale) {
+  try {
+    wpk::xent_fwd_bwd(dtype, logits, labels, loss, T, V, loss_scale, grad_scale, nullptr);
+    return sync_status("xent");
+  } catch (...) {
+    return wpc::map_exception();
+  }
+}

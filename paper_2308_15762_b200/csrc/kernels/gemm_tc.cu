@@ -223,6 +223,24 @@ CUtensorMap make_map(const Operand& op, int64_t inner, int64_t outer, int nb1, i
   return m;
 }
 
+CUtensorMap make_slab_map(const void* ptr, int dtype, int64_t cols, int64_t rows, int64_t ld) {
+  CUtensorMap m;
+  const int64_t es = dtype == kF32 ? 4 : 2;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * es)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), static_cast<cuuint32_t>(SLAB_ROWS)};
+  cuuint32_t estr[2] = {1, 1};
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * es) % 16) {
+    throw std::runtime_error("gemm epilogue map: pointer/ld must be 16-byte aligned");
+  }
+  const CUresult r = get_encoder()(&m, dtype == kF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                   2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (epilogue) failed: " + std::to_string(int(r)));
+  return m;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {

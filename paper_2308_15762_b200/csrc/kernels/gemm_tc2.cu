@@ -11,9 +11,19 @@
 //   warp 0      TMA producer (both CTAs): 6-stage ring of 32 KB stages
 //   warp 1      MMA issuer (leader only): commits multicast to both CTAs
 //   warp 2      TMEM owner (cta_group::2 alloc/dealloc in both CTAs)
-//   warps 4-7   epilogue (both CTAs): own TMEM rows -> fused op -> global;
-//               release the accumulator on the leader's barrier (8 arrivals)
+//   warps 4-11  epilogue (both CTAs): own TMEM rows -> fused op -> global;
+//               release the accumulator on the leader's barrier (16 arrivals)
+//
+// Epilogue (TE=true, every aligned problem): each epilogue warp owns a 32-row
+// x 128-column block of its CTA's 128 x 256 accumulator and moves it through
+// two 4 KB SW128 smem slabs (32 rows x 128 bytes): tcgen05.ld -> bias / GELU
+// / dGELU / residual in registers -> slab -> one TMA bulk tensor store per
+// slab (fp32 gradient accumulation uses the TMA reduce-add store, so C is
+// never read by the SM).  Residual and GELU-input tiles arrive by TMA into the
+// same slab.  Global traffic is then whole 128-byte rows per request instead
+// of one row per lane; the ring drops to 5 stages to make room (64 KB slabs).
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels/tc_common.cuh"
@@ -26,20 +36,118 @@ constexpr int PBN = 256;           // pair tile N
 constexpr int HALF_N = PBN / 2;    // columns staged per CTA
 constexpr int PM = 2 * BM;         // pair tile M
 constexpr int P_STAGE_BYTES = A_BYTES + HALF_N * BK * 2;  // 32 KB
-constexpr int P_STAGES = 6;
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr int EPI_WARPS = 8;
+constexpr int STG_BYTES = EPI_WARPS * 2 * SLAB_BYTES;  // 64 KB of epilogue slabs
 
-template <bool A_MN, bool B_MN>
+template <bool TE>
+struct PairCfg {
+  static constexpr int STAGES = TE ? 5 : 6;
+  static constexpr int SMEM_BYTES = STAGES * P_STAGE_BYTES + (TE ? STG_BYTES : 0) + 1024 + 512;
+};
+
+// One slab of the TMA epilogue: CPC accumulator columns (64 bf16 / 32 fp32)
+// of the warp's 32 rows starting at (row0, gcol); see the file header.
+template <int CPC>
+__device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map_c, const CUtensorMap* map_x,
+                                         uint8_t* slabs, uint64_t* sbar, uint32_t& sphase, int& buf, uint32_t taddr,
+                                         int gcol, int row0, int lane) {
+  const Epilogue& e = p.epi;
+  const int mode = e.mode;
+  constexpr int dt = CPC == 32 ? kF32 : kBF16;
+  const bool needs_in = mode == kEpiResidual || mode == kEpiDGelu;
+  uint8_t* sb = slabs + buf * SLAB_BYTES;
+  if (lane == 0) {
+    // the slab(s) about to be written must have been read out by earlier stores
+    if (mode == kEpiGelu) bulk_wait_read<0>();
+    else bulk_wait_read<1>();
+  }
+  __syncwarp();
+  if (needs_in && lane == 0) {
+    mbar_expect_tx(&sbar[buf], SLAB_BYTES);
+    tma_load_2d(map_x, &sbar[buf], sb, gcol, row0);
+  }
+  float v[CPC];
+  tmem_ld32(taddr, v);
+  if constexpr (CPC == 64) tmem_ld32(taddr + 32, v + 32);
+  if (e.bias && gcol + CPC <= p.N) {
+#pragma unroll
+    for (int i = 0; i < CPC; i += 4) {
+      const float4 b4 = *reinterpret_cast<const float4*>(e.bias + gcol + i);
+      v[i] = fmaf(v[i], e.alpha, b4.x), v[i + 1] = fmaf(v[i + 1], e.alpha, b4.y);
+      v[i + 2] = fmaf(v[i + 2], e.alpha, b4.z), v[i + 3] = fmaf(v[i + 3], e.alpha, b4.w);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < CPC; ++i) v[i] = v[i] * e.alpha + ((e.bias && gcol + i < p.N) ? e.bias[gcol + i] : 0.f);
+  }
+  if (needs_in) {
+    mbar_wait(&sbar[buf], (sphase >> buf) & 1);
+    sphase ^= 1u << buf;
+    float x[CPC];
+    if constexpr (CPC == 32) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = *reinterpret_cast<const float4*>(sb + slab_off(lane, q));
+        x[4 * q] = f.x, x[4 * q + 1] = f.y, x[4 * q + 2] = f.z, x[4 * q + 3] = f.w;
+      }
+    } else {
+      slab_get_bf16(sb, lane, x);
+    }
+    if (mode == kEpiResidual) {
+#pragma unroll
+      for (int i = 0; i < CPC; ++i) v[i] += x[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < CPC; ++i) v[i] *= gelu_grad_fast(x[i]);
+    }
+  }
+  auto put = [&](uint8_t* slab) {
+    if constexpr (CPC == 32) slab_put_f32(slab, lane, v);
+    else slab_put_bf16(slab, lane, v);
+  };
+  if (mode == kEpiGelu) {
+    uint8_t* sg = slabs + (buf ^ 1) * SLAB_BYTES;
+#pragma unroll
+    for (int i = 0; i < CPC; ++i) v[i] = round_to(dt, v[i]);  // GELU of the stored pre-activation
+    put(sb);
+#pragma unroll
+    for (int i = 0; i < CPC; ++i) v[i] = gelu_fast(v[i]);
+    put(sg);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(map_x, sb, gcol, row0);
+      tma_store_2d(map_c, sg, gcol, row0);
+      bulk_commit();
+    }
+  } else {
+    put(sb);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if (mode == kEpiAccum) tma_reduce_add_2d(map_c, sb, gcol, row0);
+      else tma_store_2d(map_c, sb, gcol, row0);
+      bulk_commit();
+    }
+    buf ^= 1;
+  }
+}
+
+template <bool A_MN, bool B_MN, bool TE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_x,
                     const __grid_constant__ Params p) {
+  constexpr int P_STAGES = PairCfg<TE>::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint8_t* stg = smem + P_STAGES * P_STAGE_BYTES;  // epilogue slabs (TE)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + (TE ? STG_BYTES : 0));
   uint64_t* empty_bar = full_bar + P_STAGES;
   uint64_t* tfull_bar = empty_bar + P_STAGES;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* slab_bar = tempty_bar + 2;         // [EPI_WARPS][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slab_bar + 2 * EPI_WARPS);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -60,6 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 16);  // 8 epilogue warps x 2 CTAs (leader's copy is used)
     }
+    for (int i = 0; i < 2 * EPI_WARPS; ++i) mbar_init(&slab_bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -140,6 +249,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         tc_commit_pair(&tfull_bar[acc]);  // both halves of the accumulator ready
       }
     }
+  } else if (warp >= 4 && TE) {
+    const int ew = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const bool f32 = p.epi.mode == kEpiAccum || p.epi.c_dtype == kF32;
+    const int cpc = f32 ? 32 : 64;  // columns per slab
+    uint8_t* slabs = stg + (warp - 4) * 2 * SLAB_BYTES;
+    uint64_t* sbar = slab_bar + (warp - 4) * 2;
+    uint32_t sphase = 0;
+    int buf = 0;
+    int local = 0;
+    for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
+      int mb, nb, z1, z2;
+      decode_tile(p, t, mb, nb, z1, z2);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row0 = mb * PM + static_cast<int>(rank) * BM + ew * 32;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * PBN;
+      for (int c = half * (PBN / 2); c < (half + 1) * (PBN / 2); c += cpc) {
+        const int gcol = nb * PBN + c;
+        if (gcol >= p.N) break;
+        if (f32) epi_slab<32>(p, &map_c, &map_x, slabs, sbar, sphase, buf, taddr + c, gcol, row0, lane);
+        else epi_slab<64>(p, &map_c, &map_x, slabs, sbar, sphase, buf, taddr + c, gcol, row0, lane);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 0);
+    }
+    if (lane == 0) bulk_wait<0>();
   } else if (warp >= 4) {
     const int ew = warp & 3;
     const int half = (warp - 4) >> 2;
@@ -175,21 +314,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, bool TE>
 void launch_pair(const GemmProblem& g, const Params& p, cudaStream_t s) {
-  auto* k = gemm_tc2_kernel<A_MN, B_MN>;
+  auto* k = gemm_tc2_kernel<A_MN, B_MN, TE>;
+  constexpr int SMEM = PairCfg<TE>::SMEM_BYTES;
   static uint64_t attr_done = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_done >> (dev & 63) & 1)) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr_done |= 1ull << (dev & 63);
   }
   const CUtensorMap ma = A_MN ? make_map(g.A, g.M, g.K, g.nb1, g.nb2, 64) : make_map(g.A, g.K, g.M, g.nb1, g.nb2, BM);
   const CUtensorMap mb =
       B_MN ? make_map(g.B, g.N, g.K, g.nb1, g.nb2, 64) : make_map(g.B, g.K, g.N, g.nb1, g.nb2, HALF_N);
+  CUtensorMap mc{}, mx{};
+  if (TE) {
+    const Epilogue& e = g.epi;
+    const int dt = e.mode == kEpiAccum ? kF32 : e.c_dtype;
+    mc = make_slab_map(e.c, dt, g.N, g.M, e.ldc);
+    const void* x = e.mode == kEpiResidual ? e.resid : (e.mode == kEpiGelu || e.mode == kEpiDGelu) ? e.aux : nullptr;
+    mx = x ? make_slab_map(x, dt, g.N, g.M, e.ldc) : mc;
+  }
   const int pairs = std::min(p.num_tiles, num_sms() / 2);
-  k<<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, s>>>(ma, mb, p);
+  k<<<2 * pairs, NUM_THREADS, SMEM, s>>>(ma, mb, mc, mx, p);
 }
 
 }  // namespace
@@ -197,12 +345,18 @@ void launch_pair(const GemmProblem& g, const Params& p, cudaStream_t s) {
 int gemm_tc2(const GemmProblem& g, cudaStream_t s) {
   Params p;
   fill_params(g, p, PM, PBN);
-  const int sel = (g.A.mn_major ? 2 : 0) + (g.B.mn_major ? 1 : 0);
+  static const bool te_off = std::getenv("WP_GEMM_NO_TMA_EPI") != nullptr;  // A/B switch for profiling
+  const bool te = p.vec_ok && !te_off;
+  const int sel = (g.A.mn_major ? 2 : 0) + (g.B.mn_major ? 1 : 0) + (te ? 4 : 0);
   switch (sel) {
-    case 0: launch_pair<false, false>(g, p, s); break;
-    case 1: launch_pair<false, true>(g, p, s); break;
-    case 2: launch_pair<true, false>(g, p, s); break;
-    default: launch_pair<true, true>(g, p, s); break;
+    case 0: launch_pair<false, false, false>(g, p, s); break;
+    case 1: launch_pair<false, true, false>(g, p, s); break;
+    case 2: launch_pair<true, false, false>(g, p, s); break;
+    case 3: launch_pair<true, true, false>(g, p, s); break;
+    case 4: launch_pair<false, false, true>(g, p, s); break;
+    case 5: launch_pair<false, true, true>(g, p, s); break;
+    case 6: launch_pair<true, false, true>(g, p, s); break;
+    default: launch_pair<true, true, true>(g, p, s); break;
   }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc2 launch: ") + cudaGetErrorString(e));

@@ -5,6 +5,7 @@
 // partial sums + one global atomic per column for parameter gradients.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <stdexcept>
 #include <string>
@@ -176,6 +177,80 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_k(const T* dy, const T* x, cons
   }
 }
 
+// Fused LayerNorm backward: dx (as ln_bwd_dx_k) and the dw / db partial sums
+// in one pass over dy and x.  A block owns a contiguous row range; each lane
+// keeps its 8*C columns' dw / db sums in registers across the rows its warp
+// visits, the 8 warps combine them through shared-memory atomics and the
+// block adds its partial to the global fp32 gradients (one atomic per column
+// per block).  HBM traffic per row: dy and x read once (the second pass hits
+// L1), dx (and dres) once -- the separate dw/db kernel's re-read is gone.
+template <typename T, int C>
+__global__ void __launch_bounds__(256, 1) ln_bwd_fused_k(const T* dy, const T* x, const float* mean,
+                                                         const float* rstd, const float* w, const T* dres, T* dx,
+                                                         float* dw, float* db, int T_, int h, int rows_per) {
+  extern __shared__ float red[];  // [2][h]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int i = threadIdx.x; i < 2 * h; i += blockDim.x) red[i] = 0.f;
+  float aw[C][8], ab[C][8];
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) aw[c][k] = ab[c][k] = 0.f;
+  const int r0 = blockIdx.x * rows_per, r1 = min(T_, r0 + rows_per);
+  for (int row = r0 + warp; row < r1; row += 8) {
+    const int64_t off = static_cast<int64_t>(row) * h;
+    const float mu = mean[row], rs = rstd[row];
+    float sg = 0.f, sgx = 0.f;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int col = c * 256 + lane * 8;
+      float d[8], xv[8], wv[8];
+      load8(dy + off + col, d);
+      load8(x + off + col, xv);
+      load8(w + col, wv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float g = d[k] * wv[k];
+        sg += g;
+        sgx += g * (xv[k] - mu) * rs;
+      }
+    }
+    sg = warp_sum(sg) / h;
+    sgx = warp_sum(sgx) / h;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int col = c * 256 + lane * 8;
+      float d[8], xv[8], wv[8], r[8], o[8];
+      load8(dy + off + col, d);
+      load8(x + off + col, xv);
+      load8(w + col, wv);
+      if (dres) load8(dres + off + col, r);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float xh = (xv[k] - mu) * rs;
+        o[k] = rs * (d[k] * wv[k] - sg - xh * sgx) + (dres ? r[k] : 0.f);
+        aw[c][k] += d[k] * xh;
+        ab[c][k] += d[k];
+      }
+      store8(dx + off + col, o);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      atomicAdd(&red[c * 256 + lane * 8 + k], aw[c][k]);
+      atomicAdd(&red[h + c * 256 + lane * 8 + k], ab[c][k]);
+    }
+  __syncthreads();
+  if (r0 < r1)
+    for (int i = threadIdx.x; i < h; i += blockDim.x) {
+      atomicAdd(&dw[i], red[i]);
+      atomicAdd(&db[i], red[h + i]);
+    }
+}
+
 // dw, db: lane <-> column (coalesced), 8 warps stride over a row range, block
 // partials reduced in shared memory, one atomic per column per block.
 template <typename T>
@@ -330,6 +405,80 @@ __global__ void __launch_bounds__(256) xent_k(T* logits, const int32_t* labels, 
   }
 }
 
+// Vectorised cross-entropy: XR rows per 256-thread block, 16-byte accesses.
+// Pass 1 keeps a running (max, sum) per thread, rescaling once per 8-vector
+// instead of per element; pass 2 rewrites the row with (softmax - onehot) *
+// grad_scale (the row, 100 KB at V = 50304, is still in L2).  One loss atomic
+// per block.  Needs V % 8 == 0.
+constexpr int XR = 4;
+template <typename T>
+__global__ void __launch_bounds__(256) xent_vec_k(T* logits, const int32_t* labels, float* loss, int T_, int V,
+                                                  float loss_scale, float grad_scale) {
+  __shared__ float sm[32], ss[32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  constexpr float L2E = 1.4426950408889634f;
+  float block_loss = 0.f;
+  for (int rr = 0; rr < XR; ++rr) {
+    const int row = blockIdx.x * XR + rr;
+    if (row >= T_) break;
+    T* lr = logits + static_cast<int64_t>(row) * V;
+    float m = -INFINITY, sum = 0.f;
+    for (int j = threadIdx.x * 8; j < V; j += blockDim.x * 8) {
+      float v[8];
+      load8(lr + j, v);
+      float mx = v[0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) mx = fmaxf(mx, v[k]);
+      if (mx > m) {
+        sum *= exp2f((m - mx) * L2E);
+        m = mx;
+      }
+      const float mb = m * L2E;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += exp2f(fmaf(v[k], L2E, -mb));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+      const float mm = fmaxf(m, m2);
+      sum = (m == -INFINITY ? 0.f : sum * exp2f((m - mm) * L2E)) + (m2 == -INFINITY ? 0.f : s2 * exp2f((m2 - mm) * L2E));
+      m = mm;
+    }
+    if (lane == 0) {
+      sm[warp] = m;
+      ss[warp] = sum;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      m = lane < nw ? sm[lane] : -INFINITY;
+      sum = lane < nw ? ss[lane] : 0.f;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+        const float mm = fmaxf(m, m2);
+        sum = (m == -INFINITY ? 0.f : sum * exp2f((m - mm) * L2E)) +
+              (m2 == -INFINITY ? 0.f : s2 * exp2f((m2 - mm) * L2E));
+        m = mm;
+      }
+      if (lane == 0) sm[0] = m + logf(sum);  // lse
+    }
+    __syncthreads();
+    const float lse = sm[0];
+    const int label = labels[row];
+    if (threadIdx.x == 0) block_loss += lse - to_f(lr[label]);
+    __syncthreads();  // the label logit is read before being overwritten; sm reused next row
+    const float lb = lse * L2E;
+    for (int j = threadIdx.x * 8; j < V; j += blockDim.x * 8) {
+      float v[8];
+      load8(lr + j, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = (exp2f(fmaf(v[k], L2E, -lb)) - (j + k == label ? 1.f : 0.f)) * grad_scale;
+      store8(lr + j, v);
+    }
+  }
+  if (threadIdx.x == 0) atomicAdd(loss, block_loss * loss_scale);
+}
+
 // --------------------------------------------------------------- bias grads
 // Block = 8 warps over a 256-column strip; lane owns 8 contiguous columns
 // (one 16-byte load per row for bf16), warps stride over the block's rows,
@@ -432,9 +581,42 @@ int ln_fwd_dispatch(const T* x, const float* w, const float* b, T* y, float* mea
   return 1;
 }
 
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <typename T, int C>
+void launch_ln_bwd_fused(const T* dy, const T* x, const float* mean, const float* rstd, const float* w,
+                         const T* dres, T* dx, float* dw, float* db, int T_, int h, cudaStream_t s) {
+  // One block per SM, each over a contiguous row range (a multiple of 8 rows).
+  const int blocks = std::max(1, std::min(sm_count(), (T_ + 7) / 8));
+  const int rows_per = ((T_ + blocks - 1) / blocks + 7) / 8 * 8;
+  const int grid = (T_ + rows_per - 1) / rows_per;
+  const size_t smem = 2 * size_t(h) * sizeof(float);
+  ln_bwd_fused_k<T, C><<<grid, 256, smem, s>>>(dy, x, mean, rstd, w, dres, dx, dw, db, T_, h, rows_per);
+}
+
 template <typename T>
 int ln_bwd_dispatch(const T* dy, const T* x, const float* mean, const float* rstd, const float* w, const T* dres,
                     T* dx, float* dw, float* db, int T_, int h, cudaStream_t s) {
+  bool fused = h % 256 == 0;
+  switch (fused ? h / 256 : 0) {
+    case 1: launch_ln_bwd_fused<T, 1>(dy, x, mean, rstd, w, dres, dx, dw, db, T_, h, s); break;
+    case 2: launch_ln_bwd_fused<T, 2>(dy, x, mean, rstd, w, dres, dx, dw, db, T_, h, s); break;
+    case 4: launch_ln_bwd_fused<T, 4>(dy, x, mean, rstd, w, dres, dx, dw, db, T_, h, s); break;
+    case 8: launch_ln_bwd_fused<T, 8>(dy, x, mean, rstd, w, dres, dx, dw, db, T_, h, s); break;
+    default: fused = false; break;  // h = 4096: dw/db sums would not fit in registers
+  }
+  if (fused) {
+    check_launch("layernorm_bwd (fused)");
+    return 1;
+  }
   const dim3 grid((T_ + 7) / 8), block(256);
   switch (h / 256) {
     case 1: ln_bwd_dx_k<T, 1><<<grid, block, 0, s>>>(dy, x, mean, rstd, w, dres, dx, T_, h); break;
@@ -520,10 +702,18 @@ int softmax_bwd(int dtype, const float* dP, void* P, int rows, int n, float scal
 
 int xent_fwd_bwd(int dtype, void* logits, const int32_t* labels, float* loss, int T_, int V, float loss_scale,
                  float grad_scale, cudaStream_t s) {
-  if (dtype == kBF16)
+  if (V % 8 == 0) {
+    const int grid = (T_ + XR - 1) / XR;
+    if (dtype == kBF16)
+      xent_vec_k<bf16><<<grid, 256, 0, s>>>(static_cast<bf16*>(logits), labels, loss, T_, V, loss_scale, grad_scale);
+    else
+      xent_vec_k<float><<<grid, 256, 0, s>>>(static_cast<float*>(logits), labels, loss, T_, V, loss_scale,
+                                             grad_scale);
+  } else if (dtype == kBF16) {
     xent_k<bf16><<<T_, 256, 0, s>>>(static_cast<bf16*>(logits), labels, loss, V, loss_scale, grad_scale);
-  else
+  } else {
     xent_k<float><<<T_, 256, 0, s>>>(static_cast<float*>(logits), labels, loss, V, loss_scale, grad_scale);
+  }
   check_launch("xent");
   return 1;
 }

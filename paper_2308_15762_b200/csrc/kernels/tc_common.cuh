@@ -327,8 +327,82 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
+// --- TMA epilogue: registers -> swizzled smem slab -> bulk tensor store ----
+// A slab is 32 rows x 128 bytes (64 bf16 or 32 fp32 columns) in the SW128
+// layout: 16-byte chunk c of row r at r*128 + ((c ^ (r & 7)) << 4), so a warp
+// writing one chunk per lane (one row per lane) hits every bank exactly 4x.
+constexpr int SLAB_ROWS = 32;
+constexpr int SLAB_BYTES = SLAB_ROWS * 128;  // 4 KB
+
+__device__ __forceinline__ uint32_t slab_off(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+// global += smem (fp32 add performed at L2; the gradient-accumulation epilogue).
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// One lane's row of a slab: 8 chunks of 16 bytes.
+__device__ __forceinline__ void slab_put_bf16(uint8_t* slab, int r, const float* v /*64*/) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[8 * c + 2 * i], v[8 * c + 2 * i + 1]);
+    *reinterpret_cast<uint4*>(slab + slab_off(r, c)) = u;
+  }
+}
+__device__ __forceinline__ void slab_get_bf16(const uint8_t* slab, int r, float* v /*64*/) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 u = *reinterpret_cast<const uint4*>(slab + slab_off(r, c));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      v[8 * c + 2 * i] = f.x, v[8 * c + 2 * i + 1] = f.y;
+    }
+  }
+}
+__device__ __forceinline__ void slab_put_f32(uint8_t* slab, int r, const float* v /*32*/) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<float4*>(slab + slab_off(r, c)) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+}
+
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 get_encoder();
+// 2-D map over a row-major [rows, cols] matrix (leading dimension ld
+// elements) with a {128 bytes, 32 rows} box and SW128: the epilogue slab.
+CUtensorMap make_slab_map(const void* ptr, int dtype, int64_t cols, int64_t rows, int64_t ld);
 CUtensorMap make_map(const Operand& op, int64_t inner, int64_t outer, int nb1, int nb2, int box_outer);
 int num_sms();
 void fill_params(const GemmProblem& g, Params& p, int tile_m, int tile_n);

@@ -110,6 +110,25 @@ def test_tc_epilogues(mode):
     torch.testing.assert_close(out, ref, rtol=tol, atol=tol * 8)
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True)])
+@pytest.mark.parametrize("mode", [EPI_STORE, EPI_ACCUM, EPI_RESID, EPI_GELU, EPI_DGELU])
+@pytest.mark.parametrize("shape", [(320, 1000, 136), (512, 776, 128), (1024, 384, 256)])
+def test_tc_pair_tma_epilogue_ragged(a_mn, b_mn, mode, shape):
+    """CTA-pair kernel with the TMA-store epilogue: every fused mode, the
+    three operand layouts of the linear layers, ragged M / N edges (clipped
+    stores, zero-filled residual / GELU-input loads)."""
+    M, N, K = shape
+    c_dtype = torch.float32 if mode == EPI_ACCUM else torch.bfloat16
+    out, ref = run(M, N, K, a_mn, b_mn, torch.bfloat16, mode=mode, bias=mode != EPI_DGELU, c_dtype=c_dtype)
+    tol = 1e-3 if c_dtype == torch.float32 else 2e-2
+    torch.testing.assert_close(out, ref, rtol=tol, atol=tol * 8)
+
+
+def test_tc_pair_fp32_store_and_alpha():
+    out, ref = run(384, 640, 192, False, True, torch.bfloat16, c_dtype=torch.float32, alpha=0.5, bias=True)
+    torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-2)
+
+
 def test_tc_batched_alpha():
     out, ref = run(128, 128, 64, False, False, torch.bfloat16, batch=6, alpha=0.125, c_dtype=torch.float32)
     torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-2)
