@@ -188,11 +188,15 @@ def run_reference(args, rank, world):
 
 
 def workload_config(args, world):
-    return {"workload": "GPT-1.3B-like train step, Hanayo W=%d over P=%d" % (args.waves, world),
+    D = getattr(args, "replicas", 1)
+    P = world // D
+    par = f"pp{P}" + (f"xdp{D}" if D > 1 else "")
+    return {"workload": "GPT-1.3B-like train step, Hanayo W=%d over P=%d" % (args.waves, P)
+            + (f", {D} data-parallel replicas" if D > 1 else ""),
             "model": "gpt-1.3b-like", "layers": 24, "hidden": 2048, "heads": 16, "ffn": 8192, "seq_len": 1024,
             "vocab": 50304, "micro_batch_size": args.mbs, "microbatches": args.microbatches,
-            "global_batch": args.mbs * args.microbatches, "schedule": f"hanayo P={world} W={args.waves} "
-            f"B={args.microbatches}", "parallelism": f"pp{world}", "optimizer": "adamw",
+            "global_batch": args.mbs * args.microbatches * D, "schedule": f"hanayo P={P} W={args.waves} "
+            f"B={args.microbatches}" + (f" D={D}" if D > 1 else ""), "parallelism": par, "optimizer": "adamw",
             "l2_flush": "not needed: per-step working set (~35 GB) >> 126 MB L2"}
 
 
@@ -205,6 +209,8 @@ def main():
     ap.add_argument("--microbatches", type=int, default=8)
     ap.add_argument("--mbs", type=int, default=8)
     ap.add_argument("--waves", type=int, default=2)
+    ap.add_argument("--replicas", type=int, default=1,
+                    help="data-parallel replicas D (world = P*D ranks; IPC transport, peer-memory grad all-reduce)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gemm-report", action="store_true", help="per-shape GEMM table on stderr")
     args = ap.parse_args()
@@ -231,11 +237,16 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     args.gpus = world
+    D = args.replicas
+    if world % D:
+        raise SystemExit("--replicas must divide the number of ranks")
+    P = world // D
+    replica = rank // P
     desc = model_desc(args)
-    cfg = wp.make_config(wp.Scheme.Hanayo, world, args.microbatches, args.waves)
+    cfg = wp.make_config(wp.Scheme.Hanayo, P, args.microbatches, args.waves, D)
     sched = wp.generate_schedule(cfg)
     transport = os.environ.get("WP_TRANSPORT", "ipc")
-    if world > 1 and transport == "nccl":
+    if world > 1 and transport == "nccl" and D == 1:
         obj = [wp.runtime.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_NCCL, device_ids=[dev], rank=rank, nccl_id=obj[0])
@@ -244,7 +255,7 @@ def main():
     else:
         rt = wp.Runtime(desc, sched, device_ids=[dev])
 
-    tok_np, lab_np = synthetic_batch(args.microbatches, args.mbs, desc.seq, desc.vocab)
+    tok_np, lab_np = synthetic_batch(args.microbatches, args.mbs, desc.seq, desc.vocab, step=replica)
     tok_d = torch.from_numpy(tok_np).cuda()
     lab_d = torch.from_numpy(lab_np).cuda()
     tok_h = torch.from_numpy(tok_np).pin_memory()
@@ -272,7 +283,7 @@ def main():
             sec = float(t.item())
             lt = torch.tensor([loss], device="cpu" if share else "cuda")
             dist.all_reduce(lt)  # the loss lives on the rank holding the head slice
-            loss = float(lt.item())
+            loss = float(lt.item()) / D  # mean over replicas
         return sec, loss
 
     for _ in range(args.warmup):
@@ -303,10 +314,12 @@ def main():
     rt.set_tracing(False)
     tr = rt.trace()
     if world > 1:
-        mine = (tr.intervals[rank], [e for e in tr.comm_events if e.src_device == rank])
+        # replica 0's pipeline devices make up the measured trace of the list
+        pipe = rank % P
+        mine = (tr.intervals[pipe], [e for e in tr.comm_events if e.src_device == pipe])
         parts = [None] * world
         dist.all_gather_object(parts, mine)
-        tr = wp.build_trace([p[0] for p in parts], [e for p in parts for e in p[1]])
+        tr = wp.build_trace([p[0] for p in parts[:P]], [e for p in parts[:P] for e in p[1]])
     measured_bubble = wp.bubble_ratio(tr)
     msg_bytes = desc.tokens_per_microbatch * desc.hidden * 2
     copies = [e.arrival_time - e.post_time for e in tr.comm_events if e.arrival_time > e.post_time]
@@ -319,14 +332,14 @@ def main():
     tf, tb = statistics.mean(fwd) * 2 * args.waves, statistics.mean(bwd) * 2 * args.waves
     sim = wp.simulate(sched, wp.CostModel(tf, tb, 0.0))
     sim_bubble = wp.bubble_ratio(sim)
-    eq1 = wp.analytic_bubble_hanayo_d(world, args.waves, tf, tb, 0.0) if world >= 2 else None
+    eq1 = wp.analytic_bubble_hanayo_d(P, args.waves, tf, tb, 0.0) if P >= 2 else None
 
     if rank != 0:
         dist.barrier()  # peers' IPC mappings stay valid until every rank is done
         rt.close()
         dist.destroy_process_group()
         return
-    samples = args.microbatches * args.mbs * args.steps
+    samples = args.microbatches * args.mbs * args.steps * D
     value = samples / sec
     peaks, peaks_kind = load_peaks()
     peak_tc = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
@@ -337,7 +350,7 @@ def main():
             traffic = json.load(f).get("bytes_per_launch")
     except OSError:
         pass
-    flops_step = desc.flops_per_sample() * args.microbatches * args.mbs
+    flops_step = desc.flops_per_sample() * args.microbatches * args.mbs * D
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         v, dt, cores = cpu_port_sample(desc)

@@ -157,10 +157,15 @@ typedef struct wp_runtime wp_runtime;
  *    pipeline devices sharing one GPU, each with its own streams).
  *  WP_TRANSPORT_NCCL: one process per pipeline device (rank == device);
  *    `nccl_id` is the 128-byte ncclUniqueId broadcast by the caller.
- *  WP_TRANSPORT_IPC: one process per pipeline device (rank == device);
- *    messages are copy-engine pushes over NVLink into the receiver's
- *    CUDA-IPC-mapped landing slots, signalled by stream memory operations
- *    (no SMs spent on transfers).  After creation every rank exports
+ *  WP_TRANSPORT_IPC: one process per GPU; messages are copy-engine pushes
+ *    over NVLink into the receiver's CUDA-IPC-mapped landing slots,
+ *    signalled by stream memory operations (no SMs spent on transfers).
+ *    With list config replicas D > 1 (data parallelism, the reference's
+ *    bookkeeping-only D) the job has P * D ranks: rank =
+ *    replica * P + pipeline device, every replica runs the list on its own
+ *    microbatches and OptimizerStep first all-reduces (averages) the
+ *    gradients of each stage across the D replicas with one peer-memory
+ *    kernel over NVLink.  After creation every rank exports
  *    wp_runtime_ipc_handle, the caller all-gathers the handles (rank order)
  *    and passes them to wp_runtime_ipc_connect before the first step.
  *    `nccl_id` is ignored. */
@@ -171,8 +176,8 @@ int wp_runtime_create(const wp_model_desc* model, const wp_list* list, int trans
                       wp_runtime** out);
 void wp_runtime_free(wp_runtime* rt);
 /* IPC transport handshake.  `out` receives WP_IPC_HANDLE_BYTES bytes;
- * `handles` holds nranks of them, rank-major. */
-#define WP_IPC_HANDLE_BYTES 64
+ * `handles` holds nranks (= P * D) of them, rank-major. */
+#define WP_IPC_HANDLE_BYTES 128
 int wp_runtime_ipc_handle(wp_runtime* rt, void* out);
 int wp_runtime_ipc_connect(wp_runtime* rt, const void* handles, int nranks);
 /* ncclGetUniqueId for rank 0 of a WP_TRANSPORT_NCCL job (128 bytes). */

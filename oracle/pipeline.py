@@ -208,15 +208,23 @@ def run_local(desc, params, per_device, placement, B, tokens, labels):
     return devs
 
 
-def run_dist(desc, params, per_device, placement, B, tokens, labels):
+def run_dist(desc, params, per_device, placement, B, tokens, labels, replicas=1):
     """One process per pipeline device over torch.distributed point-to-point
     (gloo on CPU), issuing communication the way the runtime's NCCL transport
     does: every incoming message of the step is posted at step start, per
     channel in the sender's order (FIFO matching, tag 0); Sends and the
     outgoing halves of BatchedExchanges are issued in program order right
-    after their producer; a consumer waits only for its own message."""
+    after their producer; a consumer waits only for its own message.
+
+    replicas = D > 1: global rank = replica * P + pipeline device (the GPU
+    runtime's IPC rank layout); each replica runs the list on its own
+    microbatches and the optimizer-step flush averages the gradients over
+    the D replicas of each pipeline device (the runtime's peer-memory
+    all-reduce, here a gloo all_reduce on a per-device group)."""
     import torch.distributed as dist
-    r = dist.get_rank()
+    P = len(per_device)
+    g = dist.get_rank()
+    r, base = g % P, (g // P) * P
     S = sum(len(x) for x in placement)
     us = units(desc)
     bounds = partition(us, S)
@@ -228,7 +236,7 @@ def run_dist(desc, params, per_device, placement, B, tokens, labels):
             continue
         for k in keys:
             buf = torch.empty(shape, dtype=torch.float64)
-            pending[k] = (dist.irecv(buf, src=src), buf)
+            pending[k] = (dist.irecv(buf, src=base + src), buf)
     sends = []
     want = dict((k, src) for src, k in incoming(per_device, r))
     for a in per_device[r]:
@@ -248,8 +256,16 @@ def run_dist(desc, params, per_device, placement, B, tokens, labels):
                 if owner(placement, consumer) == r:
                     dev.inbox[key] = dev.outbox.pop(key)
         elif k in (SEND, BATCHED_EXCHANGE):
-            sends.append(dist.isend(dev.outbox.pop(key_of(a)).contiguous(), dst=a[4]))
+            sends.append(dist.isend(dev.outbox.pop(key_of(a)).contiguous(), dst=base + a[4]))
     for q in sends:
         q.wait()
+    if replicas > 1:
+        # every rank creates every group, in the same order (collective)
+        groups = [dist.new_group([q * P + d for q in range(replicas)]) for d in range(P)]
+        for name, prm in sorted(dev.P.items()):
+            if prm.grad is not None:
+                dist.all_reduce(prm.grad, group=groups[r])
+                prm.grad /= replicas
+        dev.loss /= replicas
     assert not pending and set(want) <= set(dev.inbox) | set(want), "unconsumed messages"
     return dev

@@ -634,6 +634,24 @@ int ln_bwd_dispatch(const T* dy, const T* x, const float* mean, const float* rst
   return 2;
 }
 
+// One-shot all-reduce (mean) of this replica's share; float4 granules, fixed
+// summation order (replica 0..D-1) so every replica stores the same bits.
+constexpr int kMaxReplicas = 16;
+__global__ void allreduce_mean_k(float* const* bufs, int D, int64_t lo4, int64_t hi4, float scale) {
+  float4* b[kMaxReplicas];
+  for (int r = 0; r < D; ++r) b[r] = reinterpret_cast<float4*>(bufs[r]);
+  for (int64_t i = lo4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < hi4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 acc = b[0][i];
+    for (int r = 1; r < D; ++r) {
+      const float4 v = b[r][i];
+      acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+    }
+    acc.x *= scale, acc.y *= scale, acc.z *= scale, acc.w *= scale;
+    for (int r = 0; r < D; ++r) b[r][i] = acc;
+  }
+}
+
 }  // namespace
 
 #define WP_DISPATCH(dtype, F, ...) \
@@ -697,6 +715,18 @@ int softmax_bwd(int dtype, const float* dP, void* P, int rows, int n, float scal
   if (dtype == kBF16) softmax_bwd_k<bf16><<<grid, 256, 0, s>>>(dP, static_cast<bf16*>(P), rows, n, scale, causal);
   else softmax_bwd_k<float><<<grid, 256, 0, s>>>(dP, static_cast<float*>(P), rows, n, scale, causal);
   check_launch("softmax_bwd");
+  return 1;
+}
+
+int allreduce_mean_peers(float* const* bufs, int D, int me, int64_t n, cudaStream_t s) {
+  if (D < 1 || D > kMaxReplicas) throw std::runtime_error("allreduce: 1 <= replicas <= 16");
+  if (n % 4) throw std::runtime_error("allreduce: length must be a multiple of 4");
+  const int64_t n4 = n / 4, per = (n4 + D - 1) / D;
+  const int64_t lo = std::min(n4, per * me), hi = std::min(n4, lo + per);
+  if (hi <= lo) return 0;
+  const int grid = static_cast<int>(std::min<int64_t>(4 * sm_count(), (hi - lo + 255) / 256));
+  allreduce_mean_k<<<grid, 256, 0, s>>>(bufs, D, lo, hi, 1.0f / D);
+  check_launch("allreduce_mean_peers");
   return 1;
 }
 

@@ -92,6 +92,17 @@ void Pool::release(const BufPtr& b, cudaStream_t stream) {
 Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, int transport, const int* device_ids,
                  int rank, const void* nccl_id)
     : m_(ModelSpec::from_desc(desc)), list_(list), transport_(transport), rank_(rank) {
+  // IPC transport: `rank` is the global rank replica * P + pipeline device.
+  replicas_ = std::max(1, list_.config.replicas);
+  if (transport_ == WP_TRANSPORT_IPC) {
+    if (rank < 0 || rank >= list_.config.devices * replicas_) {
+      throw wavepipe::ConfigError("IPC transport needs 0 <= rank < P * D");
+    }
+    replica_ = rank / list_.config.devices;
+    rank_ = rank % list_.config.devices;
+  } else if (replicas_ > 1) {
+    throw wavepipe::ConfigError("data-parallel replicas (D > 1) need the IPC transport");
+  }
   const auto rep = wavepipe::validate_all(list_);
   if (!rep.ok()) {
     throw wavepipe::ScheduleError("action list fails validation:\n" + wavepipe::render_diagnostics_text(rep));
@@ -105,9 +116,6 @@ Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, in
   }
   if (transport_ != WP_TRANSPORT_LOCAL && transport_ != WP_TRANSPORT_NCCL && transport_ != WP_TRANSPORT_IPC) {
     throw wavepipe::ConfigError("unknown transport");
-  }
-  if (transport_ == WP_TRANSPORT_IPC && (rank_ < 0 || rank_ >= P)) {
-    throw wavepipe::ConfigError("IPC transport needs 0 <= rank < P");
   }
   if (transport_ == WP_TRANSPORT_NCCL && (rank_ < 0 || rank_ >= P || !nccl_id)) {
     throw wavepipe::ConfigError("NCCL transport needs 0 <= rank < P and an ncclUniqueId");
@@ -946,6 +954,7 @@ void Runtime::backward(DeviceState& d, const Action& a) {
 }
 
 void Runtime::optimizer(DeviceState& d) {
+  if (replicas_ > 1) dp_allreduce(d);
   if (!update_) return;
   wpk::OptimArgs o{m_.optimizer, m_.lr, m_.beta1, m_.beta2, m_.eps, m_.weight_decay, step_ + 1};
   launches_ += wpk::optimizer_step(o, d.master, d.grad, d.m, d.v, d.shadow, d.nparam, d.compute);

@@ -11,7 +11,8 @@
 // compute only on its own inputs.
 //
 // Layout of rank r's arena (one cudaMalloc, exported with cudaIpcGetMemHandle):
-//   [ arrive[0..M) | free[0..M) ]  32-bit flags, M = messages of the list
+//   [ arrive[0..M) | free[0..M) | ready[0..D) | done[0..D) ]  32-bit flags,
+//       M = messages of the list, D = data-parallel replicas
 //   [ landing slot of every message whose receiver is r ]
 // arrive[m] lives with the receiver (the sender's copy stream writes the
 // epoch after the copy; the receiver's compute stream waits on it), free[m]
@@ -34,7 +35,7 @@ void Runtime::ipc_setup() {
     for (const Action& a : list_.per_device[p])
       if (a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange) msgs[message_key(a)] = {p, a.peer};
   const size_t bytes = (message_bytes() + 255) & ~size_t(255);
-  ipc_flag_bytes_ = ((2 * msgs.size() * sizeof(uint32_t)) + 4095) & ~size_t(4095);
+  ipc_flag_bytes_ = ((2 * (msgs.size() + replicas_) * sizeof(uint32_t)) + 4095) & ~size_t(4095);
   // Slot offsets inside every receiver's arena (each rank derives all of
   // them: a sender needs the offset in its peer's arena).
   std::vector<size_t> off(P, ipc_flag_bytes_);
@@ -58,35 +59,54 @@ void Runtime::ipc_setup() {
       d.tx[m.dst] = s;
     }
   }
-  ipc_peer_.assign(P, nullptr);
+  ipc_peer_.assign(size_t(P) * replicas_, nullptr);
+  dp_grads_.assign(replicas_, nullptr);
+  dp_grads_[replica_] = d.grad;
 }
 
 void Runtime::ipc_handle(void* out64) const {
   if (transport_ != WP_TRANSPORT_IPC) throw wavepipe::ConfigError("runtime does not use the IPC transport");
-  static_assert(sizeof(cudaIpcMemHandle_t) == WP_IPC_HANDLE_BYTES, "IPC handle size");
+  static_assert(2 * sizeof(cudaIpcMemHandle_t) == WP_IPC_HANDLE_BYTES, "IPC handle size");
   DevGuard g(devs_[0]->cuda);
-  cudaIpcMemHandle_t h;
-  ck(cudaIpcGetMemHandle(&h, ipc_arena_), "cudaIpcGetMemHandle");
-  std::memcpy(out64, &h, sizeof(h));
+  cudaIpcMemHandle_t h[2];
+  ck(cudaIpcGetMemHandle(&h[0], ipc_arena_), "cudaIpcGetMemHandle (arena)");
+  ck(cudaIpcGetMemHandle(&h[1], devs_[0]->grad), "cudaIpcGetMemHandle (grads)");
+  std::memcpy(out64, h, sizeof(h));
 }
 
 void Runtime::ipc_connect(const void* handles, int nranks) {
   if (transport_ != WP_TRANSPORT_IPC) throw wavepipe::ConfigError("runtime does not use the IPC transport");
-  if (nranks != list_.config.devices) throw wavepipe::ConfigError("ipc_connect: need one handle per rank");
+  if (nranks != list_.config.devices * replicas_) {
+    throw wavepipe::ConfigError("ipc_connect: need one handle per rank (P * D)");
+  }
   if (ipc_connected_) throw wavepipe::ConfigError("ipc_connect called twice");
   DevGuard g(devs_[0]->cuda);
-  std::vector<uint8_t> peer(nranks, 0);
+  auto open = [&](int q, int which) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + size_t(q) * WP_IPC_HANDLE_BYTES + which * sizeof(h),
+                sizeof(h));
+    void* p = nullptr;
+    ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    return p;
+  };
+  // Pipeline neighbours inside this replica.
+  std::vector<uint8_t> peer(list_.config.devices, 0);
   for (const IpcMsg& m : ipc_msgs_) {
     if (m.src == rank_) peer[m.dst] = 1;
     if (m.dst == rank_) peer[m.src] = 1;
   }
-  for (int q = 0; q < nranks; ++q) {
-    if (!peer[q] || q == rank_) continue;
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, static_cast<const char*>(handles) + size_t(q) * sizeof(h), sizeof(h));
-    void* p = nullptr;
-    ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-    ipc_peer_[q] = static_cast<char*>(p);
+  for (int q = 0; q < list_.config.devices; ++q)
+    if (peer[q] && q != rank_) ipc_peer_[grank(replica_, q)] = static_cast<char*>(open(grank(replica_, q), 0));
+  // The same pipeline device in every other replica: flags and gradients.
+  for (int r = 0; r < replicas_; ++r) {
+    if (r == replica_) continue;
+    ipc_peer_[grank(r, rank_)] = static_cast<char*>(open(grank(r, rank_), 0));
+    dp_grads_[r] = static_cast<float*>(open(grank(r, rank_), 1));
+  }
+  if (replicas_ > 1) {
+    ck(cudaMalloc(&dp_grads_dev_, sizeof(float*) * replicas_), "cudaMalloc dp table");
+    ck(cudaMemcpy(dp_grads_dev_, dp_grads_.data(), sizeof(float*) * replicas_, cudaMemcpyHostToDevice),
+       "dp table");
   }
   ipc_connected_ = true;
 }
@@ -99,6 +119,11 @@ void Runtime::ipc_release() {
     if (p) cudaIpcCloseMemHandle(p);
     p = nullptr;
   }
+  for (int r = 0; r < static_cast<int>(dp_grads_.size()); ++r)
+    if (r != replica_ && dp_grads_[r]) cudaIpcCloseMemHandle(dp_grads_[r]);
+  dp_grads_.clear();
+  if (dp_grads_dev_) cudaFree(dp_grads_dev_);
+  dp_grads_dev_ = nullptr;
   if (ipc_arena_) cudaFree(ipc_arena_);
   ipc_arena_ = nullptr;
 }
@@ -113,7 +138,7 @@ void Runtime::ipc_send(DeviceState& d, const Action& a) {
   if (it == d.outbox.end()) throw wavepipe::SimulationError("runtime: send before its producer");
   const int m = ipc_index_.at(out);
   const IpcMsg& msg = ipc_msgs_[m];
-  char* peer = ipc_peer_.at(msg.dst);
+  char* peer = ipc_peer_.at(grank(replica_, msg.dst));
   if (!peer) throw wavepipe::ConfigError("IPC peer not connected");
   cudaStream_t s = d.tx.at(msg.dst);
   ck(cudaStreamWaitEvent(s, d.outbox_ready[out], 0), "wait ready");
@@ -141,7 +166,7 @@ void Runtime::ipc_send(DeviceState& d, const Action& a) {
 void Runtime::ipc_expect(DeviceState& d, const MsgKey& k) {
   const int m = ipc_index_.at(k);
   const IpcMsg& msg = ipc_msgs_[m];
-  char* peer = ipc_peer_.at(msg.src);
+  char* peer = ipc_peer_.at(grank(replica_, msg.src));
   if (!peer) throw wavepipe::ConfigError("IPC peer not connected");
   auto b = std::make_shared<Buf>();
   b->p = ipc_arena_ + msg.data_off;
@@ -151,6 +176,25 @@ void Runtime::ipc_expect(DeviceState& d, const MsgKey& k) {
   b->ipc_epoch = epoch_;
   d.inbox[k] = b;
   d.pending_flags.push_back(ipc_arrive_flag(ipc_arena_, m));
+}
+
+// Gradient all-reduce across the D replicas of this pipeline device, on the
+// compute stream right before the optimizer (the flush): publish "my grads
+// are final" to every replica, wait for theirs, run one peer-memory kernel
+// in which each replica averages its 1/D share over all D buffers (NVLink
+// loads) and writes the mean back into all of them (NVLink stores), then
+// publish / wait "done" so no buffer is reused while a peer still reads it.
+void Runtime::dp_allreduce(DeviceState& d) {
+  cudaStream_t s = d.compute;
+  for (int r = 0; r < replicas_; ++r)
+    if (r != replica_) StreamOps::write(s, ipc_dp_flag(ipc_peer_[grank(r, rank_)], 0, replica_), epoch_);
+  for (int r = 0; r < replicas_; ++r)
+    if (r != replica_) StreamOps::wait_geq(s, ipc_dp_flag(ipc_arena_, 0, r), epoch_);
+  launches_ += wpk::allreduce_mean_peers(dp_grads_dev_, replicas_, replica_, d.nparam, s);
+  for (int r = 0; r < replicas_; ++r)
+    if (r != replica_) StreamOps::write(s, ipc_dp_flag(ipc_peer_[grank(r, rank_)], 1, replica_), epoch_);
+  for (int r = 0; r < replicas_; ++r)
+    if (r != replica_) StreamOps::wait_geq(s, ipc_dp_flag(ipc_arena_, 1, r), epoch_);
 }
 
 }  // namespace wprt

@@ -214,9 +214,20 @@ class Runtime {
   std::vector<IpcMsg> ipc_msgs_;
   char* ipc_arena_ = nullptr;
   size_t ipc_flag_bytes_ = 0, ipc_arena_bytes_ = 0;
-  std::vector<char*> ipc_peer_;  // rank -> mapped arena (nullptr: not a neighbour)
+  std::vector<char*> ipc_peer_;  // global rank -> mapped arena (nullptr: not a peer)
   bool ipc_connected_ = false;
   uint32_t epoch_ = 0;
+  // Data-parallel replicas (list config D > 1, IPC transport only): global
+  // rank = replica * P + pipeline device.  The arena's flag region also holds
+  // ready[D] / done[D] for the gradient all-reduce of this pipeline device.
+  int replicas_ = 1, replica_ = 0;
+  std::vector<float*> dp_grads_;     // replica -> that replica's grad buffer (mapped; own = local)
+  float** dp_grads_dev_ = nullptr;   // same table in device memory (kernel argument)
+  int grank(int replica, int pipe) const { return replica * list_.config.devices + pipe; }
+  uint32_t* ipc_dp_flag(char* base, int which, int replica) const {
+    return reinterpret_cast<uint32_t*>(base) + 2 * ipc_msgs_.size() + which * replicas_ + replica;
+  }
+  void dp_allreduce(DeviceState& d);
   void ipc_setup();
   void ipc_release();
   uint32_t* ipc_arrive_flag(char* base, int m) const { return reinterpret_cast<uint32_t*>(base) + m; }

@@ -16,7 +16,7 @@ from .schedule import ActionList, SimTrace
 TRANSPORT_LOCAL = 0
 TRANSPORT_NCCL = 1
 TRANSPORT_IPC = 2
-IPC_HANDLE_BYTES = 64
+IPC_HANDLE_BYTES = 128
 
 
 @dataclass
@@ -80,9 +80,12 @@ class Runtime:
     """wp_runtime_create / wp_train_step.  transport:
     TRANSPORT_LOCAL  all pipeline devices in this process (device_ids[d] per device);
     TRANSPORT_NCCL   one process per pipeline device, NCCL send/recv (nccl_id);
-    TRANSPORT_IPC    one process per pipeline device, copy-engine pushes into
-                     CUDA-IPC-mapped landing slots; `exchange(bytes) -> [bytes]*P`
-                     all-gathers the handles (default: torch.distributed)."""
+    TRANSPORT_IPC    one process per GPU, copy-engine pushes into CUDA-IPC-mapped
+                     landing slots; with schedule.config.replicas = D > 1 the job
+                     has P*D ranks (rank = replica*P + pipeline device) and the
+                     optimizer step all-reduces gradients across replicas over
+                     peer memory; `exchange(bytes) -> [bytes]*(P*D)` all-gathers
+                     the handles (default: torch.distributed)."""
 
     def __init__(self, model: ModelDesc, schedule: ActionList, transport=TRANSPORT_LOCAL, device_ids=None,
                  rank=0, nccl_id=None, exchange=None):
@@ -105,10 +108,11 @@ class Runtime:
             mine = C.create_string_buffer(IPC_HANDLE_BYTES)
             check(lib.wp_runtime_ipc_handle(self._h, mine))
             blobs = (exchange or _all_gather_bytes)(mine.raw)
-            if len(blobs) != P or any(len(b) != IPC_HANDLE_BYTES for b in blobs):
-                raise ValueError("exchange must return one 64-byte handle per rank")
-            allh = C.create_string_buffer(b"".join(blobs), P * IPC_HANDLE_BYTES)
-            check(lib.wp_runtime_ipc_connect(self._h, allh, P))
+            world = P * max(1, schedule.config.replicas)
+            if len(blobs) != world or any(len(b) != IPC_HANDLE_BYTES for b in blobs):
+                raise ValueError(f"exchange must return one {IPC_HANDLE_BYTES}-byte handle per rank")
+            allh = C.create_string_buffer(b"".join(blobs), world * IPC_HANDLE_BYTES)
+            check(lib.wp_runtime_ipc_connect(self._h, allh, world))
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

@@ -42,7 +42,7 @@ def _desc(dtype, optimizer="sgd"):
     return wp.ModelDesc(**TINY, dtype=dtype, optimizer=optimizer, lr=1e-3, weight_decay=0.01)
 
 
-def _run(rt, params, B, desc, steps, update):
+def _run(rt, params, B, desc, steps, update, replica=0):
     from paper_2308_15762_b200.data import synthetic_batch
     for name, t in params.items():
         try:
@@ -50,13 +50,14 @@ def _run(rt, params, B, desc, steps, update):
         except Exception:  # parameter owned by another rank
             pass
     rt.set_update(update)
-    tokens, labels = synthetic_batch(B, desc.micro_batch_size, desc.seq, desc.vocab)
+    tokens, labels = synthetic_batch(B * (replica + 1), desc.micro_batch_size, desc.seq, desc.vocab)
+    tokens, labels = tokens[B * replica:], labels[B * replica:]  # replica r: microbatches [rB, (r+1)B)
     losses = [rt.train_step(tokens, labels) for _ in range(steps)]
     grads = {n: rt.get_grad(n, k) for n, k in rt.param_names()}
     return losses, grads
 
 
-def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q):
+def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q, D=1):
     import faulthandler
     import sys
     import torch.distributed as dist
@@ -71,25 +72,28 @@ def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q):
         dev = rank % ngpu
         torch.cuda.set_device(dev)
         desc = _desc(dtype, optimizer)
-        sched = wp.generate_schedule(wp.make_config(wp.Scheme.Hanayo, world, B, W))
+        P = world // D
+        sched = wp.generate_schedule(wp.make_config(wp.Scheme.Hanayo, P, B, W, D))
         rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_IPC, device_ids=[dev], rank=rank)
         params = om.init_params(desc, seed=21)
-        losses, grads = _run(rt, params, B, desc, steps, update)
+        replica = rank // P
+        losses, grads = _run(rt, params, B, desc, steps, update, replica=replica)
         all_losses = [None] * world
         dist.all_gather_object(all_losses, losses)
         rt.close()
-        q.put((rank, [sum(x) for x in zip(*all_losses)], grads))
+        # loss: sum over the pipeline devices of a replica, mean over replicas
+        q.put((rank, [sum(x) / D for x in zip(*all_losses)], grads))
     except Exception as e:  # surface the failure to the parent
         q.put((rank, repr(e), None))
     finally:
         dist.destroy_process_group()
 
 
-def _spawn(world, B, W, dtype, optimizer="sgd", steps=1, update=False):
+def _spawn(world, B, W, dtype, optimizer="sgd", steps=1, update=False, D=1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, B, W, dtype, optimizer, steps, update, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, B, W, dtype, optimizer, steps, update, q, D))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -111,6 +115,29 @@ def _spawn(world, B, W, dtype, optimizer="sgd", steps=1, update=False):
     for _, g in out.values():
         grads.update(g)
     return losses, grads
+
+
+def _spawn_raw(world, B, W, dtype, optimizer="sgd", steps=1, update=False, D=1):
+    """Per-rank (losses, grads) of a spawned job."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, B, W, dtype, optimizer, steps, update, q, D))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    try:
+        for _ in range(world):
+            rank, losses, grads = q.get(timeout=200)
+            assert grads is not None, f"rank {rank} failed: {losses}"
+            out[rank] = (losses, grads)
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    return out
 
 
 def _single_process(world, B, W, dtype, optimizer="sgd", steps=1, update=False):
@@ -152,4 +179,36 @@ def test_ipc_bf16_adamw_three_steps_follow_single_process():
     losses, _ = _spawn(2, 4, 2, "bf16", optimizer="adamw", steps=3, update=True)
     ref, _, _ = _single_process(2, 4, 2, "bf16", optimizer="adamw", steps=3, update=True)
     assert np.allclose(losses, ref, rtol=1e-3, atol=0), (losses, ref)
+    assert losses[2] < losses[0]
+
+
+@pytest.mark.parametrize("P,D,B,W", [(1, 2, 4, 2), (2, 2, 4, 2), (1, 3, 2, 1)])
+def test_data_parallel_replicas_equal_sequential_big_batch(P, D, B, W):
+    """D replicas x P pipeline devices (rank = replica*P + device): replica r
+    runs microbatches [rB, (r+1)B); the peer-memory all-reduce at the
+    optimizer step averages the gradients, so every replica holds the
+    gradient of sequential accumulation over all D*B microbatches (fp32,
+    1e-5 vs the fp64 oracle) -- the same in every replica."""
+    from oracle import model as om
+    from paper_2308_15762_b200.data import synthetic_batch
+    world = P * D
+    out = _spawn_raw(world, B, W, "fp32", D=D)
+    desc = _desc("fp32")
+    params = om.init_params(desc, seed=21)
+    tokens, labels = synthetic_batch(B * D, desc.micro_batch_size, desc.seq, desc.vocab)
+    want_loss, want = om.reference_step(params, tokens, labels, desc)
+    assert abs(out[0][0][0] - want_loss) <= 1e-5 * abs(want_loss)
+    for rank, (_, grads) in out.items():
+        for n, g in grads.items():
+            w = want[n].numpy().ravel().astype(np.float64)
+            e = np.linalg.norm(g - w) / max(np.linalg.norm(w), 1e-30)
+            assert e <= 1e-5, (rank, n, e)
+    # replicas hold bit-identical gradients (one summation order for all)
+    for rank, (_, grads) in out.items():
+        for n, g in grads.items():
+            assert np.array_equal(g, out[rank % P][1][n]), (rank, n)
+
+
+def test_data_parallel_bf16_adamw_steps():
+    losses = _spawn_raw(2, 4, 2, "bf16", optimizer="adamw", steps=3, update=True, D=2)[0][0]
     assert losses[2] < losses[0]

@@ -126,3 +126,48 @@ def test_gloo_world_size_2():
         p.join(timeout=120)
     results = dict(q.get(timeout=5) for _ in range(2))
     assert results == {0: True, 1: True}
+
+
+def _dp_worker(rank, world, P, D, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        d = Desc()
+        B = 4
+        params = om.init_params(d, seed=13)
+        replica = rank // P
+        tokens, labels = synthetic_batch(B * D, d.micro_batch_size, d.seq, d.vocab)
+        mine = slice(B * replica, B * (replica + 1))
+        acts, pl = schedule(P, B, 2)
+        dev = opl.run_dist(d, params, acts, pl, B, tokens[mine], labels[mine], replicas=D)
+        ref_loss, ref = om.reference_step(params, tokens, labels, d)
+        ok = True
+        for name, p in dev.P.items():
+            if p.grad is not None:
+                ok &= bool(torch.allclose(p.grad, ref[name], rtol=1e-10, atol=1e-12))
+        losses = [None] * world
+        dist.all_gather_object(losses, dev.loss)
+        # each rank holds its share of the replica-averaged loss
+        ok &= abs(sum(losses) - ref_loss) < 1e-10
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_data_parallel_replicas():
+    """P=2 pipeline devices x D=2 replicas (4 gloo processes, the runtime's
+    rank layout): replica-averaged gradients equal sequential accumulation
+    over all 2B microbatches."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    P, D = 2, 2
+    procs = [ctx.Process(target=_dp_worker, args=(r, P * D, P, D, port, q)) for r in range(P * D)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    results = dict(q.get(timeout=5) for _ in range(P * D))
+    assert results == {r: True for r in range(P * D)}
