@@ -21,7 +21,7 @@ static int debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype, const
     g.nb1 = nb1;
     g.nb2 = nb2;
     g.in_dtype = in_dtype;
-    g.causal = causal;
+    g.causal = causal < 0 ? 0 : causal;
     g.A = wpk::Operand{a, lda, a_mn != 0, a_b1, a_b2};
     g.B = wpk::Operand{b, ldb, b_mn != 0, b_b1, b_b2};
     g.epi.mode = mode;
@@ -35,6 +35,7 @@ static int debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype, const
     g.epi.resid = resid;
     g.epi.aux = aux;
     wpk::gemm(g, nullptr);
+    if (causal < 0) return WP_OK;  // async: the caller synchronises (timing)
     cudaError_t e = cudaDeviceSynchronize();
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return wpc::fail(WP_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
@@ -50,6 +51,17 @@ extern "C" int wp_debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype
                              int64_t c_b1, int64_t c_b2, const float* bias, const void* resid, void* aux) {
   return debug_gemm(M, N, K, nb1, nb2, in_dtype, a, lda, a_mn, a_b1, a_b2, b, ldb, b_mn, b_b1, b_b2, mode, alpha, c,
                     c_dtype, ldc, c_b1, c_b2, bias, resid, aux, 0);
+}
+
+// Same as wp_debug_gemm without the device synchronisation (back-to-back
+// launches on the legacy stream for timing).
+extern "C" int wp_debug_gemm_async(int M, int N, int K, int nb1, int nb2, int in_dtype, const void* a, int64_t lda,
+                                   int a_mn, int64_t a_b1, int64_t a_b2, const void* b, int64_t ldb, int b_mn,
+                                   int64_t b_b1, int64_t b_b2, int mode, float alpha, void* c, int c_dtype,
+                                   int64_t ldc, int64_t c_b1, int64_t c_b2, const float* bias, const void* resid,
+                                   void* aux) {
+  return debug_gemm(M, N, K, nb1, nb2, in_dtype, a, lda, a_mn, a_b1, a_b2, b, ldb, b_mn, b_b1, b_b2, mode, alpha, c,
+                    c_dtype, ldc, c_b1, c_b2, bias, resid, aux, -1);
 }
 
 extern "C" int wp_debug_gemm_causal(int M, int N, int K, int nb1, int nb2, int in_dtype, const void* a, int64_t lda,

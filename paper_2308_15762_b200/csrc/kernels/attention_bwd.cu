@@ -159,6 +159,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       constexpr uint32_t id_dq = id_kv | (1u << 15);
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aDO = smem_u32(sDO);
       const uint32_t aP = smem_u32(sP), aDS = smem_u32(sDS);
+      // K-major (k-step offsets in-atom) and MN-major (2 KB per 16 rows) descriptors
+      const uint64_t dK = make_desc(aK, 16, 1024), dQ = make_desc(aQ, 16, 1024), dV = make_desc(aV, 16, 1024),
+                     dDO = make_desc(aDO, 16, 1024), dP = make_desc(aP, 16, 1024), dDS = make_desc(aDS, 16, 1024);
+      const uint64_t dDOm = make_desc(aDO, ATOM, 1024), dQm = make_desc(aQ, ATOM, 1024),
+                     dDSm = make_desc(aDS, ATOM, 1024), dKm = make_desc(aK, ATOM, 1024);
       mbar_wait(kv_full, 0);
       for (int it = 0; it < n_it; ++it) {
         mbar_wait(qdo_full, it & 1);
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * ATOM + (k & 3) * 32;
-          tc_mma(tmem + kColS, make_desc(aK + off, 16, 1024), make_desc(aQ + off, 16, 1024), id_ss, k != 0);
+          tc_mma(tmem + kColS, desc_add(dK, off), desc_add(dQ, off), id_ss, k != 0);
         }
         if (it > 0) {
           mbar_wait(dq_free, (it - 1) & 1);  // dQ_{it-1} drained from the dP columns
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * ATOM + (k & 3) * 32;
-          tc_mma(tmem + kColDP, make_desc(aV + off, 16, 1024), make_desc(aDO + off, 16, 1024), id_ss, k != 0);
+          tc_mma(tmem + kColDP, desc_add(dV, off), desc_add(dDO, off), id_ss, k != 0);
         }
         tc_commit(s_full);
         mbar_wait(ds_full, it & 1);
@@ -185,17 +190,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k) {
           const uint32_t offa = (k >> 2) * ATOM + (k & 3) * 32;
-          tc_mma(tmem + kColDV, make_desc(aP + offa, 16, 1024), make_desc(aDO + k * 2048, ATOM, 1024), id_kv,
-                 (it | k) != 0);
-          tc_mma(tmem + Cfg::kColDK, make_desc(aDS + offa, 16, 1024), make_desc(aQ + k * 2048, ATOM, 1024), id_kv,
-                 (it | k) != 0);
+          tc_mma(tmem + kColDV, desc_add(dP, offa), desc_add(dDOm, k * 2048), id_kv, (it | k) != 0);
+          tc_mma(tmem + Cfg::kColDK, desc_add(dDS, offa), desc_add(dQm, k * 2048), id_kv, (it | k) != 0);
         }
         tc_commit(qdo_empty);
         // dQ = dS K (reduction over the 128 keys; dS^T tile read M-major)
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k) {
-          tc_mma(tmem + kColDP, make_desc(aDS + k * 2048, ATOM, 1024), make_desc(aK + k * 2048, ATOM, 1024), id_dq,
-                 k != 0);
+          tc_mma(tmem + kColDP, desc_add(dDSm, k * 2048), desc_add(dKm, k * 2048), id_dq, k != 0);
         }
         tc_commit(dq_full);
         tc_commit(pds_free);

@@ -133,8 +133,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             // K-major: +32 B per K=16 step inside the 128 B swizzle row.
             // MN-major: +16 rows x 128 B per K=16 step (two 8-row groups).
-            const uint64_t ad = A_MN ? make_desc(sa + k * 2048, CHUNK_BYTES, 1024) : make_desc(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_desc(sb + k * 2048, CHUNK_BYTES, 1024) : make_desc(sb + k * 32, 16, 1024);
+            const uint64_t ad = desc_add(A_MN ? make_desc(sa, CHUNK_BYTES, 1024) : make_desc(sa, 16, 1024),
+                                         A_MN ? k * 2048 : k * 32);
+            const uint64_t bd = desc_add(B_MN ? make_desc(sb, CHUNK_BYTES, 1024) : make_desc(sb, 16, 1024),
+                                         B_MN ? k * 2048 : k * 32);
             tc_mma(tmem_d, ad, bd, idesc, (kb != kb0 || k != 0));
           }
           tc_commit(&empty_bar[stage]);  // smem slot free once these MMAs retire

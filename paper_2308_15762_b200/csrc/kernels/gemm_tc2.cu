@@ -22,6 +22,7 @@
 // never read by the SM).  Residual and GELU-input tiles arrive by TMA into the
 // same slab.  Global traffic is then whole 128-byte rows per request instead
 // of one row per lane; the ring drops to 5 stages to make room (64 KB slabs).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
@@ -187,7 +188,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       for (int t = pair; t < p.num_tiles; t += npairs) {
         int mb, nb, z1, z2;
-        decode_tile(p, t, mb, nb, z1, z2);
+        decode_tile_grouped(p, t, mb, nb);
+        z1 = z2 = 0;
         const int row0 = mb * PM + static_cast<int>(rank) * BM;
         const int col0 = nb * PBN + static_cast<int>(rank) * HALF_N;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
@@ -234,11 +236,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * P_STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
+          const uint64_t ad0 = A_MN ? make_desc(sa, CHUNK_BYTES, 1024) : make_desc(sa, 16, 1024);
+          const uint64_t bd0 = B_MN ? make_desc(sb, CHUNK_BYTES, 1024) : make_desc(sb, 16, 1024);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = A_MN ? make_desc(sa + k * 2048, CHUNK_BYTES, 1024) : make_desc(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_desc(sb + k * 2048, CHUNK_BYTES, 1024) : make_desc(sb + k * 32, 16, 1024);
-            tc_mma_pair(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            tc_mma_pair(tmem_d, desc_add(ad0, A_MN ? k * 2048 : k * 32), desc_add(bd0, B_MN ? k * 2048 : k * 32), idesc,
+                        (kb | k) != 0);
           }
           tc_commit_pair(&empty_bar[stage]);  // frees this stage in both CTAs
           if (++stage == P_STAGES) {
@@ -261,7 +264,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int local = 0;
     for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
       int mb, nb, z1, z2;
-      decode_tile(p, t, mb, nb, z1, z2);
+      decode_tile_grouped(p, t, mb, nb);
+        z1 = z2 = 0;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -285,7 +289,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int local = 0;
     for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
       int mb, nb, z1, z2;
-      decode_tile(p, t, mb, nb, z1, z2);
+      decode_tile_grouped(p, t, mb, nb);
+        z1 = z2 = 0;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -345,6 +350,8 @@ void launch_pair(const GemmProblem& g, const Params& p, cudaStream_t s) {
 int gemm_tc2(const GemmProblem& g, cudaStream_t s) {
   Params p;
   fill_params(g, p, PM, PBN);
+  static const int gm_env = std::getenv("WP_GEMM_GROUP_M") ? std::atoi(std::getenv("WP_GEMM_GROUP_M")) : 8;
+  p.group_m = std::max(1, std::min(gm_env, p.tiles_m));
   static const bool te_off = std::getenv("WP_GEMM_NO_TMA_EPI") != nullptr;  // A/B switch for profiling
   const bool te = p.vec_ok && !te_off;
   const int sel = (g.A.mn_major ? 2 : 0) + (g.B.mn_major ? 1 : 0) + (te ? 4 : 0);

@@ -35,6 +35,7 @@ struct Params {
   int tiles_m, tiles_n, num_tiles, k_blocks;
   int vec_ok;
   int causal;  // kCausal* (gemm.cuh): per-tile skip / K range inside each s x s block
+  int group_m;  // CTA-pair kernel: tiles are rastered in groups of group_m M-blocks (L2 reuse)
   Epilogue epi;
 };
 
@@ -130,6 +131,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(lbo_bytes >> 4) << 16) |
          (static_cast<uint64_t>(sbo_bytes >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// Descriptor of the same layout `bytes` further on (start-address field only;
+// offsets stay inside shared memory, so the 14-bit field never carries).
+__device__ __forceinline__ uint64_t desc_add(uint64_t desc, uint32_t bytes) { return desc + (bytes >> 4); }
+
+// Grouped raster (single batch element): consecutive tile ids walk the
+// group_m M-blocks of a group fastest, then N, then the next group, so the
+// tiles in flight at once (one per SM pair) share a few A and B panels that
+// stay in L2 instead of streaming every A panel from DRAM once per N-block.
+__device__ __forceinline__ void decode_tile_grouped(const Params& p, int t, int& m_blk, int& n_blk) {
+  const int per_group = p.group_m * p.tiles_n;
+  const int g = t / per_group, first = g * p.group_m;
+  const int gm = min(p.tiles_m - first, p.group_m);
+  const int r = t - g * per_group;
+  m_blk = first + r % gm;
+  n_blk = r / gm;
 }
 
 __device__ __forceinline__ void decode_tile(const Params& p, int t, int& m_blk, int& n_blk, int& z1, int& z2) {

@@ -12,10 +12,11 @@ import torch  # noqa: E402
 from paper_2308_15762_b200 import _native  # noqa: E402
 
 lib = _native.lib
-lib.wp_debug_gemm.restype = C.c_int
-lib.wp_debug_gemm.argtypes = [C.c_int] * 6 + [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int64] * 2 + \
-    [C.c_int, C.c_float, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
-     C.c_void_p]
+for _f in (lib.wp_debug_gemm, lib.wp_debug_gemm_async):
+    _f.restype = C.c_int
+    _f.argtypes = [C.c_int] * 6 + [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int64] * 2 + \
+        [C.c_int, C.c_float, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+         C.c_void_p]
 
 
 def bench(M, N, K, a_mn=False, b_mn=False, iters=20):
@@ -25,13 +26,12 @@ def bench(M, N, K, a_mn=False, b_mn=False, iters=20):
     args = (M, N, K, 1, 1, 1, a.data_ptr(), M if a_mn else K, int(a_mn), 0, 0,
             b.data_ptr(), N if b_mn else K, int(b_mn), 0, 0, 0, 1.0, c.data_ptr(), 1, N, 0, 0, None, None, None)
     assert lib.wp_debug_gemm(*args) == 0, lib.wp_last_error()
-    # time through torch's stream: launch via a non-synchronising path is not
-    # exposed, so time the synchronous call's device span with events
+    # back-to-back asynchronous launches on the default stream, like cuBLAS below
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     st.record()
     for _ in range(iters):
-        lib.wp_debug_gemm(*args)
+        lib.wp_debug_gemm_async(*args)
     en.record()
     torch.cuda.synchronize()
     ms = st.elapsed_time(en) / iters
