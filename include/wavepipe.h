@@ -204,6 +204,10 @@ int wp_get_param(wp_runtime* rt, const char* name, float* host_out, int64_t nume
 int wp_set_param(wp_runtime* rt, const char* name, const float* host_in, int64_t numel);
 int wp_get_grad(wp_runtime* rt, const char* name, float* host_out, int64_t numel);
 
+/* Device memory held by this process's pipeline devices: the stash /
+ * message pool (grows to its steady state in the first step) and the IPC
+ * landing slots (bytes). */
+int wp_runtime_memory(const wp_runtime* rt, int64_t* pool_bytes, int64_t* landing_bytes);
 /* Number of this library's kernels launched since the runtime was created. */
 int wp_runtime_launch_count(const wp_runtime* rt, int64_t* launches);
 /* GEMM profiling: CUDA events around every tcgen05/SIMT GEMM launch on its

@@ -104,6 +104,7 @@ _SIGS = {
     "wp_set_param": (I, [P, C.c_char_p, C.POINTER(C.c_float), C.c_int64]),
     "wp_get_grad": (I, [P, C.c_char_p, C.POINTER(C.c_float), C.c_int64]),
     "wp_runtime_launch_count": (I, [P, I64P]),
+    "wp_runtime_memory": (I, [P, I64P, I64P]),
     "wp_runtime_set_profiling": (I, [P, I]),
     "wp_runtime_gemm_stats": (I, [P, I64P, DP, DP]),
     "wp_runtime_gemm_report": (I, [P, C.c_char_p, I]),

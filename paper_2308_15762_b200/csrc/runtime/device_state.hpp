@@ -35,6 +35,14 @@ inline MsgKey message_key(const wavepipe::Action& a) {
                 act ? (out ? a.slice_index : a.slice_index - 1) : (out ? a.slice_index - 1 : a.slice_index)};
 }
 
+// The message a compute consumes: Forward of slice s takes the activation
+// of boundary s-1, Backward of slice s the gradient of boundary s.
+inline MsgKey input_key(const wavepipe::Action& a) {
+  return a.kind == ActionKind::Forward
+             ? MsgKey{static_cast<int>(wavepipe::Payload::Activation), a.microbatch, a.slice_index - 1}
+             : MsgKey{static_cast<int>(wavepipe::Payload::Gradient), a.microbatch, a.slice_index};
+}
+
 struct DevGuard {
   int prev = 0;
   explicit DevGuard(int d) {
@@ -76,9 +84,11 @@ struct DeviceState {
   // receives (landing buffer + arrival event per message).
   std::map<int, cudaStream_t> tx, rx;
   std::map<MsgKey, std::pair<BufPtr, cudaEvent_t>> posted;
-  // IPC transport: arrival flags (local memory) the next compute must see
-  // reach this step's epoch before it starts.
-  std::vector<uint32_t*> pending_flags;
+  // IPC transport: messages whose landing slot the next compute copies out
+  // (after its arrival flag reaches the step epoch), and the stream that
+  // writes "posted" flags into senders' arenas.
+  std::vector<std::pair<MsgKey, int>> pending_ipc;
+  cudaStream_t sig = nullptr;
 
   struct Rec {
     int idx;

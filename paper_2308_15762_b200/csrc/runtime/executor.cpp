@@ -69,11 +69,7 @@ BufPtr Pool::alloc(size_t bytes, cudaStream_t stream, int cls) {
 
 void Pool::release(const BufPtr& b, cudaStream_t stream) {
   if (!b) return;
-  if (b->pool_class == 2) {
-    // IPC landing slot: hand it back to its sender for the next step.
-    StreamOps::write(stream, b->ipc_free_remote, b->ipc_epoch);
-    return;
-  }
+
   // Message buffers and anything released off the compute stream carry an
   // event: the next owner (possibly another stream or device) waits on it.
   if (b->pool_class == 1 || stream != home_) {
@@ -969,8 +965,7 @@ bool Runtime::advance(DeviceState& d) {
     if (a.is_compute()) {
       for (cudaEvent_t e : d.pending) ck(cudaStreamWaitEvent(d.compute, e, 0), "wait arrival");
       d.pending.clear();
-      for (uint32_t* f : d.pending_flags) StreamOps::wait_geq(d.compute, f, epoch_);
-      d.pending_flags.clear();
+      if (!d.pending_ipc.empty()) ipc_land(d, a);
       d.last_start = next_event(d);
       ck(cudaEventRecord(d.last_start, d.compute), "record start");
       if (a.kind == ActionKind::Forward) forward(d, a);
@@ -984,12 +979,12 @@ bool Runtime::advance(DeviceState& d) {
       optimizer(d);
     } else if (transport_ == WP_TRANSPORT_IPC) {
       if (a.kind == ActionKind::Receive) {
-        ipc_expect(d, message_key(a));
+        ipc_post(d, message_key(a));
       } else {
         ipc_send(d, a);
         if (a.kind == ActionKind::BatchedExchange) {
           const auto [q, qi] = d.be_partner[d.pc];
-          ipc_expect(d, message_key(list_.per_device[q][qi]));
+          ipc_post(d, message_key(list_.per_device[q][qi]));
         }
       }
     } else if (transport_ == WP_TRANSPORT_NCCL) {
@@ -1086,6 +1081,7 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     throw wavepipe::ConfigError("IPC transport: call ipc_connect with every rank's handle before the first step");
   }
   epoch_ = static_cast<uint32_t>(step_ + 1);
+  for (auto& kv : ipc_send_next_) kv.second = 0;
   const size_t n = size_t(list_.config.microbatches) * m_.tokens();
   for (auto& d : devs_) {
     DevGuard g(d->cuda);
@@ -1099,7 +1095,7 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     d->pc = 0;
     d->ev_next = 0;
     d->pending.clear();
-    d->pending_flags.clear();
+    d->pending_ipc.clear();
     d->last_start = nullptr;
     d->recs.clear();
     d->comm_recs.clear();
@@ -1121,7 +1117,7 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     ck(cudaMemcpy(&l, d->loss, sizeof(float), cudaMemcpyDeviceToHost), "loss D2H");
     loss += l;
     if (!d->stash.empty() || !d->handoff.empty() || !d->inbox.empty() || !d->outbox.empty() ||
-        !d->posted.empty()) {
+        !d->posted.empty() || !d->pending_ipc.empty() || !ipc_ready_.empty()) {
       throw wavepipe::SimulationError("runtime: state left over at the end of the step");
     }
   }
@@ -1177,6 +1173,13 @@ void Runtime::collect_trace() {
               return std::tie(x.arrival_time, x.post_time, x.src_device, x.dst_device) <
                      std::tie(y.arrival_time, y.post_time, y.src_device, y.dst_device);
             });
+}
+
+void Runtime::memory(int64_t* pool_bytes, int64_t* landing_bytes) const {
+  int64_t pool = 0;
+  for (const auto& d : devs_) pool += static_cast<int64_t>(d->pool->reserved());
+  *pool_bytes = pool;
+  *landing_bytes = ipc_arena_ ? static_cast<int64_t>(ipc_arena_bytes_ - ipc_flag_bytes_) : 0;
 }
 
 std::string Runtime::gemm_report() const {

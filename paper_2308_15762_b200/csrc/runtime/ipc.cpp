@@ -4,20 +4,26 @@
 //
 // Reference semantics kept (src/simulate.cpp:117-155): a Send is buffered --
 // it fires once its producer is done and never blocks the sender's compute
-// stream; a Receive / the incoming half of a BatchedExchange gates only the
-// next compute of the receiver.  The deadlock-freedom argument is the
-// reference's buffered replay (src/validate.cpp:438-495): a send waits only
-// on its producer and on the previous step's release of its own slot, a
-// compute only on its own inputs.
+// stream; a Receive is *posted* at the start of the compute preceding its
+// consumer (depth-1 prefetch, :123-133) and the bytes move at max(post,
+// fire); the arrival gates only the consumer.  The incoming half of a
+// BatchedExchange is posted the same way.  A send waits only on its producer
+// and on its post, a compute only on its inputs -- the buffered replay of
+// src/validate.cpp:438-495, hence deadlock-free.
+//
+// Memory: a landing slot is occupied from its post to the start of the
+// consumer, which copies it into a stash buffer of the runtime's pool (the
+// buffer the reference's memory_profile counts, src/analytics.cpp:61-76).
+// Slots are assigned statically by walking each receiver's program (every
+// rank derives every assignment, so a sender knows the slot address in its
+// peer's arena) and reused as soon as the previous occupant was copied out:
+// one or two slots per GPU instead of one per message.
 //
 // Layout of rank r's arena (one cudaMalloc, exported with cudaIpcGetMemHandle):
-//   [ arrive[0..M) | free[0..M) | ready[0..D) | done[0..D) ]  32-bit flags,
-//       M = messages of the list, D = data-parallel replicas
-//   [ landing slot of every message whose receiver is r ]
-// arrive[m] lives with the receiver (the sender's copy stream writes the
-// epoch after the copy; the receiver's compute stream waits on it), free[m]
-// lives with the sender (the receiver's stream writes the epoch when the
-// slot is released, i.e. when the consuming slice's stash entry dies).
+//   [ arrive[0..M) | posted[0..M) | ready[0..D) | done[0..D) ]  32-bit flags,
+//       M = messages of the list, D = data-parallel replicas;
+//       arrive[m] is used when r receives m, posted[m] when r sends m
+//   [ landing slots of r ]
 #include <cstring>
 
 #include "runtime/device_state.hpp"
@@ -34,24 +40,69 @@ void Runtime::ipc_setup() {
   for (int p = 0; p < P; ++p)
     for (const Action& a : list_.per_device[p])
       if (a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange) msgs[message_key(a)] = {p, a.peer};
-  const size_t bytes = (message_bytes() + 255) & ~size_t(255);
-  ipc_flag_bytes_ = ((2 * (msgs.size() + replicas_) * sizeof(uint32_t)) + 4095) & ~size_t(4095);
-  // Slot offsets inside every receiver's arena (each rank derives all of
-  // them: a sender needs the offset in its peer's arena).
-  std::vector<size_t> off(P, ipc_flag_bytes_);
   for (auto& [k, sd] : msgs) {
     ipc_index_[k] = static_cast<int>(ipc_msgs_.size());
-    ipc_msgs_.push_back(IpcMsg{sd.first, sd.second, off[sd.second]});
-    off[sd.second] += bytes;
+    ipc_msgs_.push_back(IpcMsg{sd.first, sd.second, -1, 0});
   }
-  ipc_arena_bytes_ = std::max<size_t>(off[rank_], 4096);
+  // Landing-slot assignment per receiver, in its program order: message m is
+  // posted at the start of the compute before the Receive (post index =
+  // computes seen - 1) and copied out at the start of its consumer compute.
+  // A slot is reusable by a post at compute c once its occupant was copied
+  // out at a compute <= c (the copy-out is enqueued before c's start event).
+  ipc_slots_.assign(P, 0);
+  for (int p = 0; p < P; ++p) {
+    const auto& prog = list_.per_device[p];
+    std::map<MsgKey, int> consumer;  // input key -> compute index of its consumer
+    for (int i = 0, c = 0; i < static_cast<int>(prog.size()); ++i)
+      if (prog[i].is_compute()) consumer[input_key(prog[i])] = c++;
+    std::vector<int> free_at;  // slot -> compute index of its last copy-out
+    int computes = 0;
+    auto assign = [&](const MsgKey& k) {
+      const int post = computes - 1;
+      if (ipc_msgs_[ipc_index_.at(k)].src == rank_) ipc_send_order_[p].push_back(ipc_index_.at(k));
+      auto cit = consumer.find(k);
+      if (cit == consumer.end()) throw wavepipe::SimulationError("IPC transport: received message has no consumer");
+      const int consume = cit->second;
+      int slot = -1;
+      for (int s = 0; s < static_cast<int>(free_at.size()) && slot < 0; ++s)
+        if (free_at[s] <= post) slot = s;
+      if (slot < 0) {
+        slot = static_cast<int>(free_at.size());
+        free_at.push_back(consume);
+      }
+      free_at[slot] = consume;
+      ipc_msgs_[ipc_index_.at(k)].slot = slot;
+    };
+    for (size_t i = 0; i < prog.size(); ++i) {
+      const Action& a = prog[i];
+      if (a.is_compute()) {
+        ++computes;
+      } else if (a.kind == ActionKind::Receive) {
+        assign(message_key(a));
+      } else if (a.kind == ActionKind::BatchedExchange) {
+        // the counterpart's outgoing message (ref include/wavepipe/action.hpp:67-73)
+        for (int q = 0; q < P; ++q)
+          for (const Action& b : list_.per_device[q])
+            if (b.kind == ActionKind::BatchedExchange && b.batch_group == a.batch_group && q != p)
+              assign(message_key(b));
+      }
+    }
+    ipc_slots_[p] = static_cast<int>(free_at.size());
+  }
+  const size_t bytes = (message_bytes() + 255) & ~size_t(255);
+  ipc_flag_bytes_ = ((2 * (ipc_msgs_.size() + replicas_) * sizeof(uint32_t)) + 4095) & ~size_t(4095);
+  for (IpcMsg& m : ipc_msgs_) {
+    if (m.slot < 0) throw wavepipe::SimulationError("IPC transport: message without a receive");
+    m.data_off = ipc_flag_bytes_ + size_t(m.slot) * bytes;
+  }
+  ipc_arena_bytes_ = ipc_flag_bytes_ + size_t(ipc_slots_[rank_]) * bytes;
   DeviceState& d = *devs_[0];
   DevGuard g(d.cuda);
   StreamOps::get();  // fail at creation, not mid-step, if the driver lacks stream memory ops
   ck(cudaMalloc(&ipc_arena_, ipc_arena_bytes_), "cudaMalloc IPC arena");
   ck(cudaMemset(ipc_arena_, 0, ipc_flag_bytes_), "memset IPC flags");
   ck(cudaDeviceSynchronize(), "IPC arena init");
-  // One outgoing copy stream per peer this rank sends to.
+  // One outgoing copy stream per peer this rank sends to; one signal stream.
   for (const IpcMsg& m : ipc_msgs_) {
     if (m.src == rank_ && !d.tx.count(m.dst)) {
       cudaStream_t s;
@@ -59,6 +110,7 @@ void Runtime::ipc_setup() {
       d.tx[m.dst] = s;
     }
   }
+  ck(cudaStreamCreateWithFlags(&d.sig, cudaStreamNonBlocking), "stream");
   ipc_peer_.assign(size_t(P) * replicas_, nullptr);
   dp_grads_.assign(replicas_, nullptr);
   dp_grads_[replica_] = d.grad;
@@ -126,56 +178,91 @@ void Runtime::ipc_release() {
   dp_grads_dev_ = nullptr;
   if (ipc_arena_) cudaFree(ipc_arena_);
   ipc_arena_ = nullptr;
+  if (devs_[0]->sig) cudaStreamDestroy(devs_[0]->sig);
+  devs_[0]->sig = nullptr;
 }
 
-// Send / outgoing half of an exchange: the per-peer copy stream waits for the
-// producer (ready event) and for the receiver's release of this slot in the
-// previous step, pushes the bytes into the peer's landing slot, then raises
-// the peer's arrival flag to this step's epoch.
+// Send / outgoing half of an exchange: the message is ready once its
+// producer's event is recorded; it is issued (ipc_flush) in the receiver's
+// post order.  Nothing here blocks the sender's compute stream.
 void Runtime::ipc_send(DeviceState& d, const Action& a) {
   const MsgKey out = message_key(a);
   auto it = d.outbox.find(out);
   if (it == d.outbox.end()) throw wavepipe::SimulationError("runtime: send before its producer");
   const int m = ipc_index_.at(out);
-  const IpcMsg& msg = ipc_msgs_[m];
-  char* peer = ipc_peer_.at(grank(replica_, msg.dst));
-  if (!peer) throw wavepipe::ConfigError("IPC peer not connected");
-  cudaStream_t s = d.tx.at(msg.dst);
-  ck(cudaStreamWaitEvent(s, d.outbox_ready[out], 0), "wait ready");
-  StreamOps::wait_geq(s, ipc_free_flag(ipc_arena_, m), epoch_ - 1);
-  cudaEvent_t t0 = nullptr;
-  if (tracing_) {
-    t0 = next_event(d);
-    ck(cudaEventRecord(t0, s), "record copy start");
-  }
-  ck(cudaMemcpyAsync(peer + msg.data_off, it->second->p, message_bytes(), cudaMemcpyDeviceToDevice, s),
-     "IPC peer copy");
-  if (tracing_) {
-    cudaEvent_t t1 = next_event(d);
-    ck(cudaEventRecord(t1, s), "record copy end");
-    d.comm_recs.push_back({msg.src, msg.dst, t0, t1, &d, &d});
-  }
-  StreamOps::write(s, ipc_arrive_flag(peer, m), epoch_);
-  d.pool->release(it->second, s);
+  ipc_ready_[m] = {it->second, d.outbox_ready[out]};
   d.outbox.erase(it);
   d.outbox_ready.erase(out);
+  ipc_flush(d, ipc_msgs_[m].dst);
 }
 
-// Receive / incoming half of an exchange: the landing slot becomes the
-// input buffer; the next compute waits for the arrival flag.
-void Runtime::ipc_expect(DeviceState& d, const MsgKey& k) {
+// Issue every ready message to `peer` that is next in its post order: the
+// per-peer copy stream waits for the producer (ready event) and for the
+// receiver's post, pushes the bytes into the peer's landing slot, then raises
+// the peer's arrival flag to this step's epoch.
+void Runtime::ipc_flush(DeviceState& d, int peer_dev) {
+  const auto& order = ipc_send_order_[peer_dev];
+  size_t& next = ipc_send_next_[peer_dev];
+  char* peer = ipc_peer_.at(grank(replica_, peer_dev));
+  if (!peer) throw wavepipe::ConfigError("IPC peer not connected");
+  cudaStream_t s = d.tx.at(peer_dev);
+  while (next < order.size()) {
+    const int m = order[next];
+    auto it = ipc_ready_.find(m);
+    if (it == ipc_ready_.end()) break;
+    const IpcMsg& msg = ipc_msgs_[m];
+    ck(cudaStreamWaitEvent(s, it->second.second, 0), "wait ready");
+    StreamOps::wait_geq(s, ipc_posted_flag(ipc_arena_, m), epoch_);
+    cudaEvent_t t0 = nullptr;
+    if (tracing_) {
+      t0 = next_event(d);
+      ck(cudaEventRecord(t0, s), "record copy start");
+    }
+    ck(cudaMemcpyAsync(peer + msg.data_off, it->second.first->p, message_bytes(), cudaMemcpyDeviceToDevice, s),
+       "IPC peer copy");
+    if (tracing_) {
+      cudaEvent_t t1 = next_event(d);
+      ck(cudaEventRecord(t1, s), "record copy end");
+      d.comm_recs.push_back({msg.src, msg.dst, t0, t1, &d, &d});
+    }
+    StreamOps::write(s, ipc_arrive_flag(peer, m), epoch_);
+    d.pool->release(it->second.first, s);
+    ipc_ready_.erase(it);
+    ++next;
+  }
+}
+
+// Receive / incoming half of an exchange: post it at the start of the compute
+// before the consumer (the last start event; step begin if none), by writing
+// the sender's posted flag from the signal stream; the consumer copies the
+// slot out when it starts (ipc_land).
+void Runtime::ipc_post(DeviceState& d, const MsgKey& k) {
   const int m = ipc_index_.at(k);
   const IpcMsg& msg = ipc_msgs_[m];
   char* peer = ipc_peer_.at(grank(replica_, msg.src));
   if (!peer) throw wavepipe::ConfigError("IPC peer not connected");
-  auto b = std::make_shared<Buf>();
-  b->p = ipc_arena_ + msg.data_off;
-  b->bytes = message_bytes();
-  b->pool_class = 2;
-  b->ipc_free_remote = ipc_free_flag(peer, m);
-  b->ipc_epoch = epoch_;
-  d.inbox[k] = b;
-  d.pending_flags.push_back(ipc_arrive_flag(ipc_arena_, m));
+  ck(cudaStreamWaitEvent(d.sig, d.last_start ? d.last_start : d.step_begin, 0), "wait post point");
+  StreamOps::write(d.sig, ipc_posted_flag(peer, m), epoch_);
+  d.pending_ipc.push_back({k, m});
+}
+
+// At the start of compute `a` (compute stream): wait for its posted input to
+// land, copy it out of the slot into a pool buffer (the stash entry), and
+// hand that buffer to the compute.  The slot is free for the next post.
+void Runtime::ipc_land(DeviceState& d, const Action& a) {
+  const MsgKey want = input_key(a);
+  for (size_t i = 0; i < d.pending_ipc.size(); ++i) {
+    const auto [k, m] = d.pending_ipc[i];
+    if (k.payload != want.payload || k.mb != want.mb || k.low != want.low) continue;
+    const IpcMsg& msg = ipc_msgs_[m];
+    StreamOps::wait_geq(d.compute, ipc_arrive_flag(ipc_arena_, m), epoch_);
+    BufPtr b = d.pool->alloc(message_bytes(), d.compute, 0);
+    ck(cudaMemcpyAsync(b->p, ipc_arena_ + msg.data_off, message_bytes(), cudaMemcpyDeviceToDevice, d.compute),
+       "IPC slot copy-out");
+    d.inbox[k] = b;
+    d.pending_ipc.erase(d.pending_ipc.begin() + static_cast<long>(i));
+    return;
+  }
 }
 
 // Gradient all-reduce across the D replicas of this pipeline device, on the

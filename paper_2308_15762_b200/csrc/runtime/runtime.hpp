@@ -41,13 +41,9 @@ namespace wprt {
 struct Buf {
   void* p = nullptr;
   size_t bytes = 0;
-  int pool_class = 0;  // 0 compute-only, 1 message, 2 IPC landing slot (not pool-owned)
+  int pool_class = 0;  // 0 compute-only, 1 message
   cudaEvent_t ev = nullptr;
   bool ev_pending = false;
-  // IPC landing slot: releasing it writes `ipc_epoch` into the sender's
-  // free flag (peer memory), letting the sender reuse the slot next step.
-  uint32_t* ipc_free_remote = nullptr;
-  uint32_t ipc_epoch = 0;
 };
 using BufPtr = std::shared_ptr<Buf>;
 
@@ -123,6 +119,9 @@ class Runtime {
   // Per GEMM shape: "MxNxK b<batch> <A,B majorness> c<causal>" -> (launches, flops, seconds).
   std::string gemm_report() const;
   int64_t launches() const { return launches_; }
+  // Device memory of the local pipeline devices: stash/message pool and the
+  // IPC landing slots (bytes).
+  void memory(int64_t* pool_bytes, int64_t* landing_bytes) const;
 
   int param_count() const { return static_cast<int>(param_index_.size()); }
   const ParamDesc& param_desc(int i, bool* owned) const;
@@ -201,15 +200,26 @@ class Runtime {
   void post_channel_receives(DeviceState& d);
 
   // CUDA-IPC transport (one process per GPU, copy-engine pushes over
-  // NVLink).  Every message of the list has a fixed landing slot in its
-  // receiver's arena and two 32-bit flags: arrive[m] in the receiver's arena
-  // (written by the sender's stream after the copy) and free[m] in the
-  // sender's arena (written by the receiver's stream when the slot is
-  // released).  Flags carry the step epoch, so nothing is reset between steps.
+  // NVLink); see ipc.cpp.  Every message m has a landing slot in its
+  // receiver's arena (statically assigned from the receiver's program order,
+  // reused as soon as the previous occupant was copied out) and two 32-bit
+  // flags carrying the step epoch: posted[m] in the sender's arena (the
+  // receiver reached the compute before the consumer, ref src/simulate.cpp:126)
+  // and arrive[m] in the receiver's arena (the bytes landed).
   struct IpcMsg {
     int src, dst;
-    size_t data_off;  // in the receiver's arena
+    int slot;         // landing slot in the receiver's arena
+    size_t data_off;  // byte offset of that slot
   };
+  std::vector<int> ipc_slots_;  // pipeline device -> landing slots of its arena
+  // Sends to each peer are copied in the order that peer posts them (its
+  // program order), so a copy waiting for its post never holds up a message
+  // the peer needs first; the host defers a produced message until every
+  // message the peer posts earlier has been issued.
+  std::map<int, std::vector<int>> ipc_send_order_;  // peer -> message ids in the peer's post order
+  std::map<int, size_t> ipc_send_next_;             // peer -> next position in that order
+  std::map<int, std::pair<BufPtr, cudaEvent_t>> ipc_ready_;  // produced, not yet issued
+  void ipc_flush(DeviceState& d, int peer);
   std::map<MsgKey, int> ipc_index_;
   std::vector<IpcMsg> ipc_msgs_;
   char* ipc_arena_ = nullptr;
@@ -231,11 +241,12 @@ class Runtime {
   void ipc_setup();
   void ipc_release();
   uint32_t* ipc_arrive_flag(char* base, int m) const { return reinterpret_cast<uint32_t*>(base) + m; }
-  uint32_t* ipc_free_flag(char* base, int m) const {
+  uint32_t* ipc_posted_flag(char* base, int m) const {
     return reinterpret_cast<uint32_t*>(base) + ipc_msgs_.size() + m;
   }
   void ipc_send(DeviceState& d, const wavepipe::Action& a);
-  void ipc_expect(DeviceState& d, const MsgKey& k);
+  void ipc_post(DeviceState& d, const MsgKey& k);
+  void ipc_land(DeviceState& d, const wavepipe::Action& a);  // at a compute's start: its input
 };
 
 }  // namespace wprt

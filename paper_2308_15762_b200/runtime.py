@@ -156,6 +156,12 @@ class Runtime:
         check(lib.wp_runtime_launch_count(self._h, C.byref(n)))
         return n.value
 
+    def memory(self):
+        """(pool_bytes, landing_bytes): stash/message pool and IPC landing slots."""
+        a, b = C.c_int64(), C.c_int64()
+        check(lib.wp_runtime_memory(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def set_profiling(self, on=True):
         check(lib.wp_runtime_set_profiling(self._h, int(on)))
 

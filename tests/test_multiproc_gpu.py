@@ -78,6 +78,11 @@ def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q, D=1):
         params = om.init_params(desc, seed=21)
         replica = rank // P
         losses, grads = _run(rt, params, B, desc, steps, update, replica=replica)
+        # landing slots are reused as soon as the consumer copied them out:
+        # at most two per GPU for the generated lists
+        msg = desc.micro_batch_size * desc.seq * desc.hidden * (4 if dtype == "fp32" else 2)
+        _, landing = rt.memory()
+        assert landing <= 2 * ((msg + 255) // 256 * 256), (landing, msg)
         all_losses = [None] * world
         dist.all_gather_object(all_losses, losses)
         rt.close()
@@ -152,7 +157,7 @@ def _single_process(world, B, W, dtype, optimizer="sgd", steps=1, update=False):
     return losses, grads, params
 
 
-@pytest.mark.parametrize("world,B,W", [(2, 4, 2), (4, 8, 2), (3, 6, 1)])
+@pytest.mark.parametrize("world,B,W", [(2, 4, 2), (4, 8, 2), (3, 6, 1), (8, 8, 2)])
 def test_ipc_fp32_equals_single_process_and_oracle(world, B, W):
     from oracle import model as om
     from paper_2308_15762_b200.data import synthetic_batch
