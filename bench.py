@@ -321,6 +321,12 @@ def main():
         dist.all_gather_object(parts, mine)
         tr = wp.build_trace([p[0] for p in parts[:P]], [e for p in parts[:P] for e in p[1]])
     measured_bubble = wp.bubble_ratio(tr)
+    pool_b, landing_b = rt.memory()
+    mem = [None] * world
+    if world > 1:
+        dist.all_gather_object(mem, (pool_b, landing_b))
+    else:
+        mem = [(pool_b, landing_b)]
     msg_bytes = desc.tokens_per_microbatch * desc.hidden * 2
     copies = [e.arrival_time - e.post_time for e in tr.comm_events if e.arrival_time > e.post_time]
     p2p = {"messages": len(tr.comm_events), "bytes_per_message": msg_bytes,
@@ -367,6 +373,9 @@ def main():
         "bubble": {"measured": measured_bubble, "simulated_at_measured_costs": sim_bubble, "eq1": eq1,
                    "t_forward_s": tf, "t_backward_s": tb},
         "p2p": p2p,
+        "memory": {"stash_pool_gb_max": max(m[0] for m in mem) / 1e9,
+                   "landing_gb_max": max(m[1] for m in mem) / 1e9,
+                   "reference_peak_activation_units": [str(u) for u in wp.memory_profile(sim, sched)[1]]},
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05, all GEMM launches of the step)",
                      "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
                      "frac": achieved / peak_tc if achieved else None, "traffic": traffic,
