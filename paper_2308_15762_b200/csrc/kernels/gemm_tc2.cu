@@ -51,7 +51,7 @@ struct PairCfg {
 template <int CPC>
 __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map_c, const CUtensorMap* map_x,
                                          uint8_t* slabs, uint64_t* sbar, uint32_t& sphase, int& buf, uint32_t taddr,
-                                         int gcol, int row0, int lane) {
+                                         int gcol, int row0, int lane, const float* bias) {
   const Epilogue& e = p.epi;
   const int mode = e.mode;
   constexpr int dt = CPC == 32 ? kF32 : kBF16;
@@ -70,16 +70,16 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
   float v[CPC];
   tmem_ld32(taddr, v);
   if constexpr (CPC == 64) tmem_ld32(taddr + 32, v + 32);
-  if (e.bias && gcol + CPC <= p.N) {
+  if (bias && gcol + CPC <= p.N) {
 #pragma unroll
     for (int i = 0; i < CPC; i += 4) {
-      const float4 b4 = *reinterpret_cast<const float4*>(e.bias + gcol + i);
+      const float4 b4 = *reinterpret_cast<const float4*>(bias + gcol + i);
       v[i] = fmaf(v[i], e.alpha, b4.x), v[i + 1] = fmaf(v[i + 1], e.alpha, b4.y);
       v[i + 2] = fmaf(v[i + 2], e.alpha, b4.z), v[i + 3] = fmaf(v[i + 3], e.alpha, b4.w);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < CPC; ++i) v[i] = v[i] * e.alpha + ((e.bias && gcol + i < p.N) ? e.bias[gcol + i] : 0.f);
+    for (int i = 0; i < CPC; ++i) v[i] = v[i] * e.alpha + ((bias && gcol + i < p.N) ? bias[gcol + i] : 0.f);
   }
   if (needs_in) {
     mbar_wait(&sbar[buf], (sphase >> buf) & 1);
@@ -186,13 +186,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < p.num_tiles; t += npairs) {
-        int mb, nb, z1, z2;
-        decode_tile_grouped(p, t, mb, nb);
-        z1 = z2 = 0;
+      for (int u = pair; u < p.num_tiles * p.k_split; u += npairs) {
+        int mb, nb, z1 = 0, z2 = 0;
+        decode_tile_grouped(p, u / p.k_split, mb, nb);
+        const int kb0 = (u % p.k_split) * p.kb_per, kb1 = min(p.k_blocks, kb0 + p.kb_per);
         const int row0 = mb * PM + static_cast<int>(rank) * BM;
         const int col0 = nb * PBN + static_cast<int>(rank) * HALF_N;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * P_STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
@@ -225,13 +225,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
+      for (int u = pair; u < p.num_tiles * p.k_split; u += npairs, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * PBN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        const int kb0 = (u % p.k_split) * p.kb_per, kb1 = min(p.k_blocks, kb0 + p.kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * P_STAGE_BYTES);
@@ -241,7 +242,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             tc_mma_pair(tmem_d, desc_add(ad0, A_MN ? k * 2048 : k * 32), desc_add(bd0, B_MN ? k * 2048 : k * 32), idesc,
-                        (kb | k) != 0);
+                        (kb != kb0 || k != 0) ? 1u : 0u);
           }
           tc_commit_pair(&empty_bar[stage]);  // frees this stage in both CTAs
           if (++stage == P_STAGES) {
@@ -262,10 +263,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint32_t sphase = 0;
     int buf = 0;
     int local = 0;
-    for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
-      int mb, nb, z1, z2;
-      decode_tile_grouped(p, t, mb, nb);
-        z1 = z2 = 0;
+    for (int u = pair; u < p.num_tiles * p.k_split; u += npairs, ++local) {
+      int mb, nb;
+      decode_tile_grouped(p, u / p.k_split, mb, nb);
+      const float* bias = u % p.k_split == 0 ? p.epi.bias : nullptr;  // split-K: bias once
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -275,8 +276,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int c = half * (PBN / 2); c < (half + 1) * (PBN / 2); c += cpc) {
         const int gcol = nb * PBN + c;
         if (gcol >= p.N) break;
-        if (f32) epi_slab<32>(p, &map_c, &map_x, slabs, sbar, sphase, buf, taddr + c, gcol, row0, lane);
-        else epi_slab<64>(p, &map_c, &map_x, slabs, sbar, sphase, buf, taddr + c, gcol, row0, lane);
+        if (f32) epi_slab<32>(p, &map_c, &map_x, slabs, sbar, sphase, buf, taddr + c, gcol, row0, lane, bias);
+        else epi_slab<64>(p, &map_c, &map_x, slabs, sbar, sphase, buf, taddr + c, gcol, row0, lane, bias);
       }
       tc_fence_before();
       __syncwarp();
@@ -341,7 +342,7 @@ void launch_pair(const GemmProblem& g, const Params& p, cudaStream_t s) {
     const void* x = e.mode == kEpiResidual ? e.resid : (e.mode == kEpiGelu || e.mode == kEpiDGelu) ? e.aux : nullptr;
     mx = x ? make_slab_map(x, dt, g.N, g.M, e.ldc) : mc;
   }
-  const int pairs = std::min(p.num_tiles, num_sms() / 2);
+  const int pairs = std::min(p.num_tiles * std::max(1, p.k_split), num_sms() / 2);
   k<<<2 * pairs, NUM_THREADS, SMEM, s>>>(ma, mb, mc, mx, p);
 }
 
@@ -354,6 +355,27 @@ int gemm_tc2(const GemmProblem& g, cudaStream_t s) {
   p.group_m = std::max(1, std::min(gm_env, p.tiles_m));
   static const bool te_off = std::getenv("WP_GEMM_NO_TMA_EPI") != nullptr;  // A/B switch for profiling
   const bool te = p.vec_ok && !te_off;
+  // Split-K for the fp32 gradient accumulation (the TMA reduce-add epilogue
+  // makes partial tiles commutative): a 2-way split when it fills the last
+  // wave of SM pairs better (measured: deeper splits and ranges shorter than
+  // 32 K-blocks lose more to pipeline fill and fp32 reduce traffic).
+  p.k_split = 1;
+  p.kb_per = p.k_blocks;
+  static const bool split_off = std::getenv("WP_GEMM_NO_SPLITK") != nullptr;
+  if (te && !split_off && g.epi.mode == kEpiAccum) {
+    const int pairs = num_sms() / 2;
+    double best = 0.0;
+    for (int s = 1; s <= 2 && p.k_blocks / s >= 32; ++s) {
+      const int per = (p.k_blocks + s - 1) / s, parts = (p.k_blocks + per - 1) / per;
+      const int64_t units = int64_t(p.num_tiles) * parts;
+      const double eff = double(units) / (double((units + pairs - 1) / pairs) * pairs);
+      if (eff > best + 0.02) {
+        best = eff;
+        p.k_split = parts;
+        p.kb_per = per;
+      }
+    }
+  }
   const int sel = (g.A.mn_major ? 2 : 0) + (g.B.mn_major ? 1 : 0) + (te ? 4 : 0);
   switch (sel) {
     case 0: launch_pair<false, false, false>(g, p, s); break;

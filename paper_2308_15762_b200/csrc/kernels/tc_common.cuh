@@ -36,6 +36,7 @@ struct Params {
   int vec_ok;
   int causal;  // kCausal* (gemm.cuh): per-tile skip / K range inside each s x s block
   int group_m;  // CTA-pair kernel: tiles are rastered in groups of group_m M-blocks (L2 reuse)
+  int k_split, kb_per;  // CTA-pair kernel, fp32 accumulation: K split into k_split ranges of kb_per blocks
   Epilogue epi;
 };
 

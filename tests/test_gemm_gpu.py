@@ -124,6 +124,15 @@ def test_tc_pair_tma_epilogue_ragged(a_mn, b_mn, mode, shape):
     torch.testing.assert_close(out, ref, rtol=tol, atol=tol * 8)
 
 
+@pytest.mark.parametrize("shape", [(2048, 2048, 8192), (768, 512, 4096), (1024, 640, 2112)])
+def test_tc_pair_split_k_accumulation(shape):
+    """Weight-gradient shapes whose tile count underfills the last wave of SM
+    pairs run split-K: partial tiles reduce-add into the fp32 gradient."""
+    M, N, K = shape
+    out, ref = run(M, N, K, True, True, torch.bfloat16, mode=EPI_ACCUM, c_dtype=torch.float32)
+    torch.testing.assert_close(out, ref, rtol=1e-3, atol=2e-3 * K ** 0.5)
+
+
 def test_tc_pair_fp32_store_and_alpha():
     out, ref = run(384, 640, 192, False, True, torch.bfloat16, c_dtype=torch.float32, alpha=0.5, bias=True)
     torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-2)
