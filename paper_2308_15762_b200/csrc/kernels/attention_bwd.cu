@@ -29,7 +29,7 @@ using namespace tc;
 
 constexpr int T128 = 128;
 constexpr int ATOM = 128 * 64 * 2;  // SW128 atom: 128 rows x 64 bf16
-constexpr int BW_THREADS = 384;     // warps 0-3 control, 4-7 softmax, 8-11 dQ drain
+constexpr int BW_THREADS = 512;     // warps 0-3 control, 4-11 softmax (two column halves), 12-15 dQ drain
 constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256;
 
 template <int D>
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     mbar_init(qdo_full, 1);
     mbar_init(qdo_empty, 1);
     mbar_init(s_full, 1);
-    mbar_init(ds_full, 4);
+    mbar_init(ds_full, 8);
     mbar_init(pds_free, 1);
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 4);
@@ -204,9 +204,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       }
       tc_commit(dkv_done);
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < 12) {
     // -------------------------------------------------- P^T / dS^T (key rows)
+    // Two warps per TMEM lane quadrant: `half` picks query columns [64h, 64h+64).
     const int ew = warp & 3;
+    const int half = (warp - 4) >> 2;
     const int r = ew * 32 + lane;
     const uint32_t lb = static_cast<uint32_t>(ew * 32) << 16;
     for (int it = 0; it < n_it; ++it) {
@@ -214,15 +216,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       float* lse = sLse + (it & 1) * T128;
       float* dl = sDelta + (it & 1) * T128;
       const int64_t vec = (static_cast<int64_t>(b) * p.heads + head) * p.seq + qi * T128;
-      lse[r] = p.lse2[vec + r];
-      dl[r] = p.delta[vec + r];
-      named_bar(1, 128);
+      if (half == 0) lse[r] = p.lse2[vec + r];
+      else dl[r] = p.delta[vec + r];
+      named_bar(1, 256);
       mbar_wait(s_full, it & 1);
       tc_fence_after();
       if (it > 0) mbar_wait(pds_free, (it - 1) & 1);
       const bool diag = p.causal && qi == kj;
 #pragma unroll 1
-      for (int c0 = 0; c0 < T128; c0 += 32) {
+      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 32) {
         float s[32], dp[32];
         tmem_ld32(tmem + lb + kColS + c0, s);
         tmem_ld32(tmem + lb + kColDP + c0, dp);
@@ -258,8 +260,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     tc_fence_after();
     const int64_t row = static_cast<int64_t>(b) * p.seq + kj * T128 + r;
     __nv_bfloat16* out = p.dqkv + row * 3 * p.hidden + head * D;
-#pragma unroll 1
-    for (int part = 0; part < 2; ++part) {
+    {
+      const int part = half;  // half 0 writes dK, half 1 writes dV
       const uint32_t col = part ? kColDV : Cfg::kColDK;
       __nv_bfloat16* dst = out + (part ? 2 : 1) * p.hidden;
 #pragma unroll
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         }
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // ------------------------------------------------ dQ drain (query rows)
     const int ew = warp & 3;
     const int r = ew * 32 + lane;
