@@ -35,10 +35,33 @@ constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256;
 template <int D>
 struct BwCfg {
   static constexpr int TILE = T128 * D * 2;     // K, V, Q, dO tiles
-  static constexpr int PT = T128 * T128 * 2;    // P^T / dS^T tiles
-  static constexpr int SMEM = 4 * TILE + 2 * PT + 2 * 2 * T128 * 4 + 1024 + 256;
+  static constexpr int PT = T128 * T128 * 2;    // dS^T tile
+  // K, V, Q[2], dO[2], dS^T, lse/delta (single-buffered), barriers
+  static constexpr int SMEM = 6 * TILE + PT + 2 * T128 * 4 + 1024 + 256;
   static constexpr uint32_t kColDK = kColDV + D;
 };
+
+// dV += P^T dO with P^T read from tensor memory (kind::f16, A in TMEM: lane =
+// key row, 32-bit column j = queries 2j, 2j+1 packed as bf16x2).
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// 16 consecutive 32-bit TMEM columns of this warp's 32 lanes.
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
 
 struct BwParams {
   int seq, heads, n_tiles, causal, hidden;
@@ -78,23 +101,22 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + Cfg::TILE;
-  uint8_t* sQ = sV + Cfg::TILE;
-  uint8_t* sDO = sQ + Cfg::TILE;
-  uint8_t* sP = sDO + Cfg::TILE;  // P^T  [keys x queries]
-  uint8_t* sDS = sP + Cfg::PT;    // dS^T [keys x queries]
-  float* sLse = reinterpret_cast<float*>(sDS + Cfg::PT);  // [2][128]
-  float* sDelta = sLse + 2 * T128;                        // [2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sDelta + 2 * T128);
+  uint8_t* sQ = sV + Cfg::TILE;       // [2]
+  uint8_t* sDO = sQ + 2 * Cfg::TILE;  // [2]
+  uint8_t* sDS = sDO + 2 * Cfg::TILE; // dS^T [keys x queries]
+  float* sLse = reinterpret_cast<float*>(sDS + Cfg::PT);  // [128]
+  float* sDelta = sLse + T128;                            // [128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDelta + T128);
   uint64_t* kv_full = bars + 0;
-  uint64_t* qdo_full = bars + 1;
-  uint64_t* qdo_empty = bars + 2;
-  uint64_t* s_full = bars + 3;
-  uint64_t* ds_full = bars + 4;
-  uint64_t* pds_free = bars + 5;
-  uint64_t* dq_full = bars + 6;
-  uint64_t* dq_free = bars + 7;
-  uint64_t* dkv_done = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* qdo_full = bars + 1;   // [2]
+  uint64_t* qdo_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* ds_full = bars + 6;
+  uint64_t* pds_free = bars + 7;
+  uint64_t* dq_full = bars + 8;
+  uint64_t* dq_free = bars + 9;
+  uint64_t* dkv_done = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kj = static_cast<int>(blockIdx.x % p.n_tiles);  // light-to-heavy order reversed: small kj = most q tiles
@@ -109,8 +131,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   }
   if (warp == 1 && lane == 0) {
     mbar_init(kv_full, 1);
-    mbar_init(qdo_full, 1);
-    mbar_init(qdo_empty, 1);
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&qdo_full[x], 1);
+      mbar_init(&qdo_empty[x], 1);
+    }
     mbar_init(s_full, 1);
     mbar_init(ds_full, 8);
     mbar_init(pds_free, 1);
@@ -137,14 +161,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         tma_load_4d(&map_k, kv_full, sK + a * ATOM, a * 64, head, kj * T128, b);
         tma_load_4d(&map_v, kv_full, sV + a * ATOM, a * 64, head, kj * T128, b);
       }
-      for (int it = 0; it < n_it; ++it) {
-        const int qi = i0 + it;
-        if (it > 0) mbar_wait(qdo_empty, (it - 1) & 1);
-        mbar_expect_tx(qdo_full, 2 * Cfg::TILE);
+      for (int it = 0; it < n_it; ++it) {  // Q / dO double-buffered: up to two tiles ahead
+        const int qi = i0 + it, x = it & 1;
+        if (it >= 2) mbar_wait(&qdo_empty[x], ((it - 2) >> 1) & 1);
+        mbar_expect_tx(&qdo_full[x], 2 * Cfg::TILE);
 #pragma unroll
         for (int a = 0; a < D / 64; ++a) {
-          tma_load_4d(&map_q, qdo_full, sQ + a * ATOM, a * 64, head, qi * T128, b);
-          tma_load_4d(&map_do, qdo_full, sDO + a * ATOM, a * 64, head, qi * T128, b);
+          tma_load_4d(&map_q, &qdo_full[x], sQ + x * Cfg::TILE + a * ATOM, a * 64, head, qi * T128, b);
+          tma_load_4d(&map_do, &qdo_full[x], sDO + x * Cfg::TILE + a * ATOM, a * 64, head, qi * T128, b);
         }
       }
     }
@@ -157,17 +181,19 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       constexpr uint32_t id_kv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) |
                                  (uint32_t(T128 >> 4) << 24);
       constexpr uint32_t id_dq = id_kv | (1u << 15);
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aDO = smem_u32(sDO);
-      const uint32_t aP = smem_u32(sP), aDS = smem_u32(sDS);
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aDS = smem_u32(sDS);
       // K-major (k-step offsets in-atom) and MN-major (2 KB per 16 rows) descriptors
-      const uint64_t dK = make_desc(aK, 16, 1024), dQ = make_desc(aQ, 16, 1024), dV = make_desc(aV, 16, 1024),
-                     dDO = make_desc(aDO, 16, 1024), dP = make_desc(aP, 16, 1024), dDS = make_desc(aDS, 16, 1024);
-      const uint64_t dDOm = make_desc(aDO, ATOM, 1024), dQm = make_desc(aQ, ATOM, 1024),
-                     dDSm = make_desc(aDS, ATOM, 1024), dKm = make_desc(aK, ATOM, 1024);
+      const uint64_t dK = make_desc(aK, 16, 1024), dV = make_desc(aV, 16, 1024), dDS = make_desc(aDS, 16, 1024);
+      const uint64_t dDSm = make_desc(aDS, ATOM, 1024), dKm = make_desc(aK, ATOM, 1024);
       mbar_wait(kv_full, 0);
       for (int it = 0; it < n_it; ++it) {
-        mbar_wait(qdo_full, it & 1);
+        const int x = it & 1;
+        const uint32_t aQ = smem_u32(sQ + x * Cfg::TILE), aDO = smem_u32(sDO + x * Cfg::TILE);
+        const uint64_t dQ = make_desc(aQ, 16, 1024), dDO = make_desc(aDO, 16, 1024);
+        const uint64_t dDOm = make_desc(aDO, ATOM, 1024), dQm = make_desc(aQ, ATOM, 1024);
+        mbar_wait(&qdo_full[x], (it >> 1) & 1);
         tc_fence_after();
+        // (S^T overwrites the P^T(it-1) columns: issued after dV(it-1), which read them.)
         // S^T = K Q^T, dP^T = V dO^T (reduction over D)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
@@ -186,14 +212,16 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         tc_commit(s_full);
         mbar_wait(ds_full, it & 1);
         tc_fence_after();
-        // dV += P^T dO, dK += dS^T Q (reduction over the 128 queries)
+        // dV += P^T dO (P^T from TMEM: queries [0,64) at columns 0.., [64,128) at 64..),
+        // dK += dS^T Q (reduction over the 128 queries)
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k) {
           const uint32_t offa = (k >> 2) * ATOM + (k & 3) * 32;
-          tc_mma(tmem + kColDV, desc_add(dP, offa), desc_add(dDOm, k * 2048), id_kv, (it | k) != 0);
+          tc_mma_ts(tmem + kColDV, tmem + kColS + (k >> 2) * 64 + (k & 3) * 8, desc_add(dDOm, k * 2048), id_kv,
+                    (it | k) != 0);
           tc_mma(tmem + Cfg::kColDK, desc_add(dDS, offa), desc_add(dQm, k * 2048), id_kv, (it | k) != 0);
         }
-        tc_commit(qdo_empty);
+        tc_commit(&qdo_empty[x]);
         // dQ = dS K (reduction over the 128 keys; dS^T tile read M-major)
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k) {
@@ -213,9 +241,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const uint32_t lb = static_cast<uint32_t>(ew * 32) << 16;
     for (int it = 0; it < n_it; ++it) {
       const int qi = i0 + it;
-      float* lse = sLse + (it & 1) * T128;
-      float* dl = sDelta + (it & 1) * T128;
+      float* lse = sLse;
+      float* dl = sDelta;
       const int64_t vec = (static_cast<int64_t>(b) * p.heads + head) * p.seq + qi * T128;
+      if (it > 0) named_bar(1, 256);  // everyone is done with the previous tile's lse / delta
       if (half == 0) lse[r] = p.lse2[vec + r];
       else dl[r] = p.delta[vec + r];
       named_bar(1, 256);
@@ -236,20 +265,24 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           pv[i] = pr;
           ds[i] = pr * (dp[i] - dl[c]) * p.scale;
         }
+        // P^T chunk -> bf16x2 -> TMEM over this half's own S^T columns (already read)
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(pv[2 * i], pv[2 * i + 1]);
+          pk[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        tmem_st16(tmem + lb + kColS + half * 64 + (c0 - half * 64) / 2, pk);
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          uint4 up, ud;
-          __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&up);
+          uint4 ud;
           __nv_bfloat162* hd = reinterpret_cast<__nv_bfloat162*>(&ud);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            hp[i] = __floats2bfloat162_rn(pv[8 * g + 2 * i], pv[8 * g + 2 * i + 1]);
-            hd[i] = __floats2bfloat162_rn(ds[8 * g + 2 * i], ds[8 * g + 2 * i + 1]);
-          }
-          *reinterpret_cast<uint4*>(sP + swz(r, c0 / 8 + g)) = up;
+          for (int i = 0; i < 4; ++i) hd[i] = __floats2bfloat162_rn(ds[8 * g + 2 * i], ds[8 * g + 2 * i + 1]);
           *reinterpret_cast<uint4*>(sDS + swz(r, c0 / 8 + g)) = ud;
         }
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();

@@ -36,7 +36,14 @@ constexpr int QT = 128;                 // queries per tile
 constexpr int KT = 128;                 // keys per tile
 constexpr int ATOM = 128 * 64 * 2;      // one SW128 K-major atom: 128 rows x 64 bf16 = 16 KB
 constexpr int FA_THREADS = 384;         // w0 TMA, w1 TMEM + MMA, w4-7 softmax A, w8-11 softmax B
-constexpr int RING = 3;                 // K/V tile slots
+constexpr int RING = 3;                 // K/V tile slots: K_j in slot j%2, V_j in slot 2
+
+// Ring tile t: K_j = 2j, V_j = 2j+1.  K tiles alternate two slots (K_{j+1}
+// reuses K_{j-1}'s, free once both S(j-1) products are done -- early), V
+// tiles share the third (V_j reuses V_{j-1}'s, free at the end of step j-1,
+// and is needed only at the end of step j).
+__device__ __forceinline__ int ring_slot(int t) { return (t & 1) ? 2 : ((t >> 1) & 1); }
+__device__ __forceinline__ int ring_use(int t) { return (t & 1) ? (t >> 1) : (t >> 2); }
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 template <int D>
@@ -194,14 +201,22 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 #pragma unroll
         for (int a = 0; a < D / 64; ++a)
           tma_load_4d(&map_q, q_full, sQ + x * Cfg::TILE + a * ATOM, a * 64, head, qt[x] * QT, b);
-      for (int t = 0; t < 2 * n_max; ++t) {  // K_0, V_0, K_1, V_1, ...
-        const int slot = t % RING;
-        if (t >= RING) mbar_wait(&kv_empty[slot], ((t / RING) & 1) ^ 1);
+      auto load = [&](int t) {
+        const int slot = ring_slot(t), use = ring_use(t);
+        if (use > 0) mbar_wait(&kv_empty[slot], (use - 1) & 1);
         mbar_expect_tx(&kv_full[slot], Cfg::TILE);
         const CUtensorMap* m = (t & 1) ? &map_v : &map_k;
 #pragma unroll
         for (int a = 0; a < D / 64; ++a)
           tma_load_4d(m, &kv_full[slot], sR + slot * Cfg::TILE + a * ATOM, a * 64, head, (t >> 1) * KT, b);
+      };
+      // K_0, V_0, K_1, then K_{j+1} before V_j: each waits only for its own slot.
+      load(0);
+      load(1);
+      if (n_max > 1) load(2);
+      for (int j = 1; j < n_max; ++j) {
+        if (j + 1 < n_max) load(2 * (j + 1));
+        load(2 * j + 1);
       }
     } else if (warp == 1 && lane == 0) {
       // ------------------------------------------------------------- MMA
@@ -211,12 +226,12 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       constexpr uint32_t idesc_pv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) |
                                     (uint32_t(QT >> 4) << 24);
       auto tile_ready = [&](int t) -> uint32_t {  // waits for ring tile t, returns its smem address
-        const int slot = t % RING;
-        mbar_wait(&kv_full[slot], (t / RING) & 1);
+        const int slot = ring_slot(t);
+        mbar_wait(&kv_full[slot], ring_use(t) & 1);
         tc_fence_after();
         return smem_u32(sR + slot * Cfg::TILE);
       };
-      auto free_tile = [&](int t) { tc_commit(&kv_empty[t % RING]); };
+      auto free_tile = [&](int t) { tc_commit(&kv_empty[ring_slot(t)]); };
       auto issue_s = [&](int x, int j) {
         FA_TRACE(8, x, j);
         if (j > 0) {

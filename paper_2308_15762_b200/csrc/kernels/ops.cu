@@ -251,6 +251,89 @@ __global__ void __launch_bounds__(256, 1) ln_bwd_fused_k(const T* dy, const T* x
     }
 }
 
+// Column-owned LayerNorm backward: a block of h/8 threads spans one row (each
+// thread owns 8 contiguous columns -> one 16-byte access per tensor per row)
+// and walks a contiguous row range R = 4 rows at a time.  The row sums
+// (sum g, sum g*xhat with g = dy*w) are block reductions -- warp shuffles,
+// then one smem exchange per 4 rows -- and each thread keeps only its 8
+// columns' dw / db sums, so registers stay low, several blocks share an SM
+// and dy / x stream from HBM exactly once (kept in registers between the
+// reduction and the dx update).
+constexpr int LNR = 4;
+template <typename T>
+__global__ void __launch_bounds__(512, 1) ln_bwd_cols_k(const T* dy, const T* x, const float* mean, const float* rstd,
+                                                      const float* w, const T* dres, T* dx, float* dw, float* db,
+                                                      int T_, int h, int rows_per) {
+  __shared__ float red[32][2 * LNR];
+  __shared__ float tot[2 * LNR];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const int col = threadIdx.x * 8;
+  float wv[8], aw[8], ab[8];
+  load8(w + col, wv);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) aw[k] = ab[k] = 0.f;
+  const int r0 = blockIdx.x * rows_per, r1 = min(T_, r0 + rows_per);
+  const float inv_h = 1.f / h;
+  for (int rb = r0; rb < r1; rb += LNR) {
+    float d[LNR][8], xh[LNR][8], part[2 * LNR];
+#pragma unroll
+    for (int i = 0; i < LNR; ++i) {
+      const int row = rb + i;
+      part[2 * i] = part[2 * i + 1] = 0.f;
+      if (row < r1) {
+        const int64_t off = static_cast<int64_t>(row) * h + col;
+        load8(dy + off, d[i]);
+        load8(x + off, xh[i]);
+        const float mu = mean[row], rs = rstd[row];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          xh[i][k] = (xh[i][k] - mu) * rs;
+          const float g = d[i][k] * wv[k];
+          part[2 * i] += g;
+          part[2 * i + 1] += g * xh[i][k];
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2 * LNR; ++q) part[q] = warp_sum(part[q]);
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 2 * LNR; ++q) red[warp][q] = part[q];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < 2 * LNR; ++q) {
+        float v = lane < nw ? red[lane][q] : 0.f;
+        v = warp_sum(v);
+        if (lane == 0) tot[q] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < LNR; ++i) {
+      const int row = rb + i;
+      if (row >= r1) break;
+      const int64_t off = static_cast<int64_t>(row) * h + col;
+      const float rs = rstd[row], sg = tot[2 * i] * inv_h, sgx = tot[2 * i + 1] * inv_h;
+      float r[8], o[8];
+      if (dres) load8(dres + off, r);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        o[k] = rs * (d[i][k] * wv[k] - sg - xh[i][k] * sgx) + (dres ? r[k] : 0.f);
+        aw[k] += d[i][k] * xh[i][k];
+        ab[k] += d[i][k];
+      }
+      store8(dx + off, o);
+    }
+  }
+  if (r0 < r1)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      atomicAdd(&dw[col + k], aw[k]);
+      atomicAdd(&db[col + k], ab[k]);
+    }
+}
+
 // dw, db: lane <-> column (coalesced), 8 warps stride over a row range, block
 // partials reduced in shared memory, one atomic per column per block.
 template <typename T>
@@ -605,6 +688,15 @@ void launch_ln_bwd_fused(const T* dy, const T* x, const float* mean, const float
 template <typename T>
 int ln_bwd_dispatch(const T* dy, const T* x, const float* mean, const float* rstd, const float* w, const T* dres,
                     T* dx, float* dw, float* db, int T_, int h, cudaStream_t s) {
+  if (h % 256 == 0 && h / 8 <= 512) {
+    // Two blocks per SM, contiguous row ranges (multiples of LNR rows).
+    const int blocks = std::max(1, std::min(2 * sm_count(), (T_ + LNR - 1) / LNR));
+    const int rows_per = ((T_ + blocks - 1) / blocks + LNR - 1) / LNR * LNR;
+    const int grid = (T_ + rows_per - 1) / rows_per;
+    ln_bwd_cols_k<T><<<grid, h / 8, 0, s>>>(dy, x, mean, rstd, w, dres, dx, dw, db, T_, h, rows_per);
+    check_launch("layernorm_bwd (column-owned)");
+    return 1;
+  }
   bool fused = h % 256 == 0;
   switch (fused ? h / 256 : 0) {
     case 1: launch_ln_bwd_fused<T, 1>(dy, x, mean, rstd, w, dres, dx, dw, db, T_, h, s); break;
