@@ -95,7 +95,7 @@ template <int D>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     flash_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                      const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
-                     const __grid_constant__ BwParams p) {
+                     const __grid_constant__ CUtensorMap map_dq, const __grid_constant__ BwParams p) {
   using Cfg = BwCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(ds_full, 8);
-    mbar_init(pds_free, 1);
+    mbar_init(pds_free, 5);  // dQ MMA commit + the 4 drain warps' slab reads
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 4);
     mbar_init(dkv_done, 1);
@@ -313,25 +313,42 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     }
   } else if (warp >= 12) {
     // ------------------------------------------------ dQ drain (query rows)
+    // TMEM -> fp32 SW128 slabs (staged in the dS^T buffer, free once the dQ
+    // MMA that read it is done) -> TMA bulk reduce-add into dq_acc: whole
+    // 128-byte row segments reduced in L2 instead of per-lane atomics.
     const int ew = warp & 3;
-    const int r = ew * 32 + lane;
     const uint32_t lb = static_cast<uint32_t>(ew * 32) << 16;
+    uint8_t* slabs = sDS + ew * 2 * SLAB_BYTES;
     for (int it = 0; it < n_it; ++it) {
       const int qi = i0 + it;
       mbar_wait(dq_full, it & 1);
       tc_fence_after();
-      float* dst = p.dq_acc + (static_cast<int64_t>(b) * p.seq + qi * T128 + r) * p.hidden + head * D;
+      const int row0 = b * p.seq + qi * T128 + ew * 32;
 #pragma unroll 1
       for (int c = 0; c < D; c += 32) {
+        uint8_t* sb = slabs + ((c / 32) & 1) * SLAB_BYTES;
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
         float v[32];
         tmem_ld32(tmem + lb + kColDP + c, v);
-#pragma unroll
-        for (int g = 0; g < 32; g += 4) red_add_v4(dst + c + g, v[g], v[g + 1], v[g + 2], v[g + 3]);
+        slab_put_f32(sb, lane, v);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_2d(&map_dq, sb, head * D + c, row0);
+          bulk_commit();
+        }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(dq_free);
+      if (lane == 0) mbar_arrive(dq_free);  // dQ TMEM columns read out
+      if (lane == 0) {
+        bulk_wait_read<0>();
+        mbar_arrive(pds_free);  // dS^T buffer no longer read by the reduce stores
+      }
+      __syncwarp();
     }
+    if (lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -419,7 +436,8 @@ void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const flo
   p.dq_acc = dq_acc;
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   const int grid = p.n_tiles * s.heads * s.mbs;
-  k<<<grid, BW_THREADS, BwCfg<D>::SMEM, stream>>>(mq, mk, mv, mdo, p);
+  const CUtensorMap mdq = make_slab_map(dq_acc, kF32, s.hidden, int64_t(s.mbs) * s.seq, s.hidden);
+  k<<<grid, BW_THREADS, BwCfg<D>::SMEM, stream>>>(mq, mk, mv, mdo, mdq, p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("flash_attn_bwd: ") + cudaGetErrorString(e));
 }
