@@ -350,11 +350,17 @@ def main():
     peaks, peaks_kind = load_peaks()
     peak_tc = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
     achieved = g_flops / g_sec / 1e12 if g_sec > 0 else None
-    traffic = None
+    # DRAM bytes of one launch of the dominant GEMM (FC1 forward, the most
+    # expensive shape) from an ncu --set full capture (tools/gemm_traffic.py),
+    # next to its algorithmic bytes.
+    traffic, traffic_info = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
-            traffic = json.load(f).get("bytes_per_launch")
-    except OSError:
+            tj = json.load(f)
+        traffic = tj.get("bytes_per_launch")
+        traffic_info = {"shape_mnk": tj.get("shape"), "algorithmic_bytes": tj.get("algorithmic_bytes"),
+                        "ratio": tj.get("ratio")}
+    except (OSError, ValueError):
         pass
     flops_step = desc.flops_per_sample() * args.microbatches * args.mbs * D
     cpu = None
@@ -379,6 +385,7 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05, all GEMM launches of the step)",
                      "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
                      "frac": achieved / peak_tc if achieved else None, "traffic": traffic,
+                     "traffic_launch": traffic_info,
                      "peak_kind": f"{peaks_kind} bf16 sustained (kernel timed inside a long step)",
                      "gemm_launches": g_launches, "gemm_share_of_step": g_sec / (sec * 1.0)},
         "cpu_baseline": cpu,
