@@ -12,7 +12,7 @@ static int debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype, const
                              int a_mn, int64_t a_b1, int64_t a_b2, const void* b, int64_t ldb, int b_mn,
                              int64_t b_b1, int64_t b_b2, int mode, float alpha, void* c, int c_dtype, int64_t ldc,
                              int64_t c_b1, int64_t c_b2, const float* bias, const void* resid, void* aux,
-                             int causal) {
+                             int causal, float* colsum = nullptr) {
   try {
     wpk::GemmProblem g;
     g.M = M;
@@ -34,6 +34,7 @@ static int debug_gemm(int M, int N, int K, int nb1, int nb2, int in_dtype, const
     g.epi.bias = bias;
     g.epi.resid = resid;
     g.epi.aux = aux;
+    g.epi.colsum = colsum;
     wpk::gemm(g, nullptr);
     if (causal < 0) return WP_OK;  // async: the caller synchronises (timing)
     cudaError_t e = cudaDeviceSynchronize();
@@ -62,6 +63,14 @@ extern "C" int wp_debug_gemm_async(int M, int N, int K, int nb1, int nb2, int in
                                    void* aux) {
   return debug_gemm(M, N, K, nb1, nb2, in_dtype, a, lda, a_mn, a_b1, a_b2, b, ldb, b_mn, b_b1, b_b2, mode, alpha, c,
                     c_dtype, ldc, c_b1, c_b2, bias, resid, aux, -1);
+}
+
+// wp_debug_gemm plus the fused bias-gradient column sums (colsum[n] += sum of C's column n).
+extern "C" int wp_debug_gemm_colsum(int M, int N, int K, int in_dtype, const void* a, int64_t lda, int a_mn,
+                                    const void* b, int64_t ldb, int b_mn, int mode, void* c, int c_dtype,
+                                    int64_t ldc, const void* aux, float* colsum) {
+  return debug_gemm(M, N, K, 1, 1, in_dtype, a, lda, a_mn, 0, 0, b, ldb, b_mn, 0, 0, mode, 1.0f, c, c_dtype, ldc, 0,
+                    0, nullptr, nullptr, const_cast<void*>(aux), 0, colsum);
 }
 
 extern "C" int wp_debug_gemm_causal(int M, int N, int K, int nb1, int nb2, int in_dtype, const void* a, int64_t lda,

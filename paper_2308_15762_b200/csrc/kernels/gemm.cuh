@@ -46,6 +46,10 @@ struct Epilogue {
   const float* bias = nullptr;  // [N] fp32, optional
   const void* resid = nullptr;  // same dtype/ld as C (kEpiResidual)
   void* aux = nullptr;          // same dtype/ld as C (kEpiGelu out, kEpiDGelu in)
+  // Optional: colsum[n] += sum over rows of the epilogue's output (fp32, the
+  // bias gradient of the layer whose input gradient C is).  Fused into the
+  // CTA-pair kernel's epilogue; other paths add a column-sum pass.
+  float* colsum = nullptr;
 };
 
 // Causal structure inside each batch element (an s x s attention block,

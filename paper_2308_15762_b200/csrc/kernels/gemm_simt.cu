@@ -8,6 +8,7 @@
 #include <stdexcept>
 
 #include "kernels/gemm.cuh"
+#include "kernels/ops.cuh"
 
 namespace wpk {
 namespace {
@@ -135,7 +136,13 @@ int gemm_simt(const GemmProblem& g, cudaStream_t s) {
 }
 
 int gemm(const GemmProblem& g, cudaStream_t s) {
-  return g.in_dtype == kBF16 ? gemm_tc(g, s) : gemm_simt(g, s);
+  if (g.in_dtype == kBF16) return gemm_tc(g, s);
+  int n = gemm_simt(g, s);
+  if (g.epi.colsum) {
+    if (g.nb1 * g.nb2 != 1) throw std::runtime_error("gemm: colsum needs an unbatched problem");
+    n += colsum_accum(g.epi.c_dtype, g.epi.c, g.epi.colsum, g.M, g.N, static_cast<int>(g.epi.ldc), s);
+  }
+  return n;
 }
 
 }  // namespace wpk

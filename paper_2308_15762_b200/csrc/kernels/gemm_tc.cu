@@ -23,6 +23,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "kernels/ops.cuh"
 #include "kernels/tc_common.cuh"
 
 namespace wpk {
@@ -301,6 +302,13 @@ int gemm_tc(const GemmProblem& g, cudaStream_t s) {  // declared in gemm.cuh
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return 0;
   static const bool pair_off = std::getenv("WP_GEMM_NO_PAIR") != nullptr;
   if (!pair_off && g.causal == kCausalNone && g.M >= 256 && g.N > 128 && g.nb1 * g.nb2 == 1) return gemm_tc2(g, s);
+  if (g.epi.colsum) {  // unfused path: the column sums as a separate pass
+    if (g.nb1 * g.nb2 != 1) throw std::runtime_error("gemm: colsum needs an unbatched problem");
+    GemmProblem g2 = g;
+    g2.epi.colsum = nullptr;
+    const int n = gemm_tc(g2, s);
+    return n + colsum_accum(g.epi.c_dtype, g.epi.c, g.epi.colsum, g.M, g.N, static_cast<int>(g.epi.ldc), s);
+  }
   const int BN = g.N <= 128 ? 128 : 256;
   Params p;
   fill_params(g, p, BM, BN);

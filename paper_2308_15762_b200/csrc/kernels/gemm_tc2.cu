@@ -132,6 +132,30 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
     }
     buf ^= 1;
   }
+  if (e.colsum) {
+    // Column sums of this slab's 32 rows (one per lane): a transposing
+    // butterfly leaves column (32q + lane) in v[32q] after 31 shuffles per 32
+    // columns, then one atomic per column per warp (rows past M masked).
+    if (row0 + lane >= p.M)
+#pragma unroll
+      for (int i = 0; i < CPC; ++i) v[i] = 0.f;
+#pragma unroll
+    for (int q = 0; q < CPC / 32; ++q) {
+      float* w = v + 32 * q;
+#pragma unroll
+      for (int sh = 16; sh >= 1; sh >>= 1) {
+        const bool up = (lane & sh) != 0;
+#pragma unroll
+        for (int i = 0; i < sh; ++i) {
+          const float send = up ? w[i] : w[i + sh];
+          const float keep = up ? w[i + sh] : w[i];
+          w[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+        }
+      }
+      const int col = gcol + 32 * q + lane;
+      if (col < p.N) atomicAdd(e.colsum + col, w[0]);
+    }
+  }
 }
 
 template <bool A_MN, bool B_MN, bool TE>

@@ -745,13 +745,14 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   }
   // dX = dY W  (B N-major: W[k][n] with k = out features)
   auto dgrad = [&](const void* dY, int ld_dy, int n_out, const void* W, int n_in, void* dX, int mode = wpk::kEpiStore,
-                   const void* aux = nullptr) {
+                   const void* aux = nullptr, float* colsum = nullptr) {
     wpk::GemmProblem g;
     g.in_dtype = dt;
     g.M = T, g.N = n_in, g.K = n_out;
     g.A = op(dY, ld_dy, false);
     g.B = op(W, n_in, true);
     g.epi.mode = mode, g.epi.c = dX, g.epi.c_dtype = dt, g.epi.ldc = n_in, g.epi.aux = const_cast<void*>(aux);
+    g.epi.colsum = colsum;
     gemm(d, g);
   };
   // dW += dY^T X  (both operands MN-major over the token dimension)
@@ -792,11 +793,11 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   }
   if (u.kind == UnitKind::Mlp) {
     BufPtr du = act(int64_t(T) * f);
-    dgrad(dy->p, h, h, weight(d, L + "mlp.fc2.w"), f, du->p, wpk::kEpiDGelu, st.a->p);
+    // dU = (dY W2) * gelu'(U); the fc1 bias gradient (column sums of dU) in the same epilogue
+    dgrad(dy->p, h, h, weight(d, L + "mlp.fc2.w"), f, du->p, wpk::kEpiDGelu, st.a->p, grad(d, L + "mlp.fc1.b"));
     wgrad(dy->p, h, st.b->p, f, grad(d, L + "mlp.fc2.w"));
     launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "mlp.fc2.b"), T, h, h, cs);
     wgrad(du->p, f, st.ln->p, h, grad(d, L + "mlp.fc1.w"));
-    launches_ += wpk::colsum_accum(dt, du->p, grad(d, L + "mlp.fc1.b"), T, f, f, cs);
     BufPtr dln = act(int64_t(T) * h);
     dgrad(du->p, f, f, weight(d, L + "mlp.fc1.w"), h, dln->p);
     BufPtr dx = ln_bwd(dln, L + "ln2", dy);

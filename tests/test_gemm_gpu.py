@@ -133,6 +133,34 @@ def test_tc_pair_split_k_accumulation(shape):
     torch.testing.assert_close(out, ref, rtol=1e-3, atol=2e-3 * K ** 0.5)
 
 
+lib.wp_debug_gemm_colsum.restype = C.c_int
+lib.wp_debug_gemm_colsum.argtypes = [C.c_int] * 4 + [C.c_void_p, C.c_int64, C.c_int] * 2 + \
+    [C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("M,N,K", [(512, 1024, 256), (320, 1000, 128), (8192, 8192, 2048)])
+def test_gemm_fused_bias_grad_colsum(dtype, M, N, K):
+    """dU = (dY W) * gelu'(U) with colsum += sum_rows(dU) fused into the
+    epilogue (CTA-pair kernel; a separate pass elsewhere), vs torch fp32."""
+    code = 1 if dtype == torch.bfloat16 else 0
+    a = torch.randn(M, K, device="cuda").to(dtype)
+    b = torch.randn(K, N, device="cuda").to(dtype)       # W stored [K, N]: N-major B
+    aux = torch.randn(M, N, device="cuda").to(dtype)
+    c = torch.empty(M, N, device="cuda", dtype=dtype)
+    cs0 = torch.randn(N, device="cuda")
+    cs = cs0.clone()
+    st = lib.wp_debug_gemm_colsum(M, N, K, code, a.data_ptr(), K, 0, b.data_ptr(), N, 1, EPI_DGELU, c.data_ptr(),
+                                  code, N, aux.data_ptr(), cs.data_ptr())
+    assert st == 0, lib.wp_last_error().decode()
+    ref = (a.float() @ b.float()) * gelu_grad(aux.float())
+    tol = 2e-2 if code else 1e-4
+    torch.testing.assert_close(c.float(), ref, rtol=tol, atol=tol * 8)
+    # bf16 path sums the fp32 epilogue values; fp32 path sums the stored C
+    got, want = cs - cs0, ref.sum(0)
+    assert ((got - want).norm() / want.norm()).item() < (5e-3 if code else 1e-5)
+
+
 def test_tc_pair_fp32_store_and_alpha():
     out, ref = run(384, 640, 192, False, True, torch.bfloat16, c_dtype=torch.float32, alpha=0.5, bias=True)
     torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-2)
