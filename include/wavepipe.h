@@ -115,6 +115,11 @@ void wp_trace_free(wp_trace* trace);
 int wp_trace_build(int devices, const int* counts, const wp_interval* intervals, int n_events,
                    const wp_comm_event* events, wp_trace** out);
 
+/* trace_to_gantt, src/gantt.cpp:91-95: "svg" or "csv" rendering of a trace
+ * (simulated or measured); *out is a NUL-terminated string freed with
+ * wp_string_free. */
+int wp_trace_to_gantt(const wp_trace* trace, const char* format, char** out);
+
 /* bubble_ratio, src/analytics.cpp:32-46. */
 int wp_bubble_ratio(const wp_trace* trace, double* out);
 /* memory_profile, src/analytics.cpp:48-91: per device (num, den) pairs,

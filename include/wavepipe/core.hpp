@@ -232,6 +232,8 @@ struct SimTrace {
 
 SimTrace simulate(const ActionList& list, const CostModel& cost);
 std::string trace_to_json(const SimTrace& trace);
+// ref include/wavepipe/gantt.hpp:32 -- "svg" or "csv"; std::invalid_argument otherwise.
+std::string trace_to_gantt(const SimTrace& trace, const std::string& format);
 
 // ---------------------------------------------------------------------------
 // Analytics (ref include/wavepipe/analytics.hpp:35-140, hot-path subset plus

@@ -23,6 +23,7 @@
 #include <sstream>
 #include <string>
 
+#include "wavepipe/gantt.hpp"
 #include "wavepipe/analytics.hpp"
 #include "wavepipe/placement.hpp"
 #include "wavepipe/schedule.hpp"
@@ -118,6 +119,14 @@ int main(int argc, char** argv) {
       ActionList stored = parse_action_list(os.str());
       ActionList fresh = generate_schedule(stored.placement, stored.config, CostModel{});
       std::fputs(serialize_action_list(fresh).c_str(), stdout);
+      return 0;
+    }
+    if (cmd == "gantt" && argc == 4) {  // gantt <golden.json> svg|csv: the reference's own renderer
+      std::ifstream in(argv[2], std::ios::binary);
+      std::ostringstream os;
+      os << in.rdbuf();
+      ActionList stored = parse_action_list(os.str());
+      std::fputs(trace_to_gantt(simulate(stored, CostModel{}), argv[3]).c_str(), stdout);
       return 0;
     }
     if (cmd == "eq1" && argc == 7) {

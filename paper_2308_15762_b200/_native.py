@@ -84,6 +84,7 @@ _SIGS = {
     "wp_trace_comm_events": (I, [P, C.POINTER(C.POINTER(wp_comm_event)), IP]),
     "wp_trace_free": (None, [P]),
     "wp_trace_build": (I, [I, IP, C.POINTER(wp_interval), I, C.POINTER(wp_comm_event), PP]),
+    "wp_trace_to_gantt": (I, [P, C.c_char_p, C.POINTER(C.c_void_p)]),
     "wp_bubble_ratio": (I, [P, DP]),
     "wp_memory_profile": (I, [P, P, I64P, I64P]),
     "wp_analytic_bubble": (I, [I, I, D, D, D, DP]),

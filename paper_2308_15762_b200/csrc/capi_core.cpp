@@ -211,6 +211,21 @@ int wp_serialize(const wp_list* l, char** json) {
   }
 }
 
+int wp_trace_to_gantt(const wp_trace* t, const char* format, char** out) {
+  try {
+    if (!t || !format || !out) return fail(WP_ERR_CONFIG, "null argument");
+    const std::string s = wavepipe::trace_to_gantt(t->trace, format);
+    char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    *out = buf;
+    return WP_OK;
+  } catch (const std::invalid_argument& e) {
+    return fail(WP_ERR_CONFIG, e.what());
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 int wp_parse(const char* json, wp_list** out) {
   try {
     if (!json || !out) return fail(WP_ERR_CONFIG, "null argument");

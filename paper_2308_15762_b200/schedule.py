@@ -19,7 +19,7 @@ from ._native import (ConfigError, ScheduleError, check, lib, wp_action, wp_comm
 
 __all__ = [
     "Scheme", "ActionKind", "Payload", "Direction", "ScheduleConfig", "CostModel", "Action",
-    "ActionList", "TraceInterval", "CommEvent", "SimTrace", "build_trace", "make_config", "generate_schedule",
+    "ActionList", "TraceInterval", "CommEvent", "SimTrace", "build_trace", "trace_to_gantt", "make_config", "generate_schedule",
     "insert_comm", "simulate", "bubble_ratio", "memory_profile", "activation_variance",
     "analytic_bubble_hanayo", "analytic_bubble_hanayo_d", "analytic_bubble_simplified",
     "serialize_action_list", "parse_action_list", "validate_all", "ConfigError", "ScheduleError",
@@ -251,6 +251,16 @@ def build_trace(intervals, comm_events=()) -> SimTrace:
     h = C.c_void_p()
     check(lib.wp_trace_build(len(intervals), counts, ivs, len(comm_events), evs, C.byref(h)))
     return SimTrace(h)
+
+
+def trace_to_gantt(trace: SimTrace, fmt: str = "svg") -> str:
+    """trace_to_gantt (ref src/gantt.cpp:91-95): "svg" or "csv" text."""
+    out = C.c_void_p()
+    check(lib.wp_trace_to_gantt(trace._h, fmt.encode(), C.byref(out)))
+    try:
+        return C.string_at(out).decode()
+    finally:
+        lib.wp_string_free(out)
 
 
 def simulate(lst: ActionList, cost: CostModel = None) -> SimTrace:

@@ -12,6 +12,10 @@ reference's own src/*.cpp compiled in place by oracle/Makefile.  Outputs:
                                   bubble, memory peaks/weights, message counts, and
                                   the full streams + trace for small configs.
 
+  tests/golden/gantt/<name>.{csv,svg}
+                                  the reference's trace_to_gantt of each golden's
+                                  simulated trace (src/gantt.cpp:91-95)
+
 Usage:  make -C oracle && python tests/golden/make_golden.py
 """
 import gzip
@@ -100,5 +104,20 @@ def main():
     print(f"wrote {len(records)} grid records")
 
 
+def gantt():
+    os.makedirs(os.path.join(HERE, "gantt"), exist_ok=True)
+    for name, *_ in GOLDENS:
+        for fmt in ("csv", "svg"):
+            out = subprocess.run([DRIVER, "gantt", os.path.join(HERE, name + ".json"), fmt], check=True,
+                                 capture_output=True, text=True).stdout
+            with open(os.path.join(HERE, "gantt", f"{name}.{fmt}"), "w") as f:
+                f.write(out)
+    print(f"wrote gantt fixtures for {len(GOLDENS)} goldens")
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["gantt"]:
+        gantt()
+    else:
+        main()
+        gantt()
