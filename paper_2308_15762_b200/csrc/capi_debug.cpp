@@ -145,3 +145,27 @@ extern "C" int wp_debug_xent(int dtype, void* logits, const int32_t* labels, flo
     return wpc::map_exception();
   }
 }
+
+#include "capi_internal.hpp"
+#include "runtime/runtime.hpp"
+
+// Host-only plan of the IPC transport for a list (no GPU): landing slots per
+// device (`slots[devices]`), message count, and each message's
+// (src, dst, slot) in `msgs[3 * n]` when non-null.  For CPU tests.
+extern "C" int wp_debug_ipc_plan(const wp_list* list, int* slots, int* n_msgs, int* msgs, int capacity) {
+  try {
+    if (!list || !slots || !n_msgs) return wpc::fail(WP_ERR_CONFIG, "null argument");
+    const wprt::IpcPlan plan = wprt::make_ipc_plan(list->list);
+    for (size_t p = 0; p < plan.slots.size(); ++p) slots[p] = plan.slots[p];
+    *n_msgs = static_cast<int>(plan.msgs.size());
+    if (msgs)
+      for (int i = 0; i < *n_msgs && i < capacity; ++i) {
+        msgs[3 * i] = plan.msgs[i].src;
+        msgs[3 * i + 1] = plan.msgs[i].dst;
+        msgs[3 * i + 2] = plan.msgs[i].slot;
+      }
+    return WP_OK;
+  } catch (...) {
+    return wpc::map_exception();
+  }
+}

@@ -26,23 +26,6 @@ inline void ckn(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw wpc::CudaError(std::string(what) + ": " + NcclApi::get().GetErrorString(r));
 }
 
-// Message identity (payload, microbatch, lower slice of the boundary), the
-// reference's matching key (src/schedule.cpp:315-324, src/simulate.cpp:39-46).
-inline MsgKey message_key(const wavepipe::Action& a) {
-  const bool act = a.payload == static_cast<int>(wavepipe::Payload::Activation);
-  const bool out = a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange;
-  return MsgKey{a.payload, a.microbatch,
-                act ? (out ? a.slice_index : a.slice_index - 1) : (out ? a.slice_index - 1 : a.slice_index)};
-}
-
-// The message a compute consumes: Forward of slice s takes the activation
-// of boundary s-1, Backward of slice s the gradient of boundary s.
-inline MsgKey input_key(const wavepipe::Action& a) {
-  return a.kind == ActionKind::Forward
-             ? MsgKey{static_cast<int>(wavepipe::Payload::Activation), a.microbatch, a.slice_index - 1}
-             : MsgKey{static_cast<int>(wavepipe::Payload::Gradient), a.microbatch, a.slice_index};
-}
-
 struct DevGuard {
   int prev = 0;
   explicit DevGuard(int d) {

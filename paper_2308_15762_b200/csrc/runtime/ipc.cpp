@@ -33,33 +33,37 @@ namespace wprt {
 
 using wavepipe::Action;
 
-void Runtime::ipc_setup() {
-  // Global message table from the full list (identical on every rank).
-  const int P = list_.config.devices;
+IpcPlan make_ipc_plan(const wavepipe::ActionList& list) {
+  IpcPlan plan;
+  const int P = list.config.devices;
   std::map<MsgKey, std::pair<int, int>> msgs;  // key -> (src, dst)
+  std::map<int, std::vector<std::pair<int, int>>> groups;  // batch_group -> (device, position)
   for (int p = 0; p < P; ++p)
-    for (const Action& a : list_.per_device[p])
+    for (int i = 0; i < static_cast<int>(list.per_device[p].size()); ++i) {
+      const Action& a = list.per_device[p][i];
       if (a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange) msgs[message_key(a)] = {p, a.peer};
+      if (a.kind == ActionKind::BatchedExchange) groups[a.batch_group].push_back({p, i});
+    }
   for (auto& [k, sd] : msgs) {
-    ipc_index_[k] = static_cast<int>(ipc_msgs_.size());
-    ipc_msgs_.push_back(IpcMsg{sd.first, sd.second, -1, 0});
+    plan.index[k] = static_cast<int>(plan.msgs.size());
+    plan.msgs.push_back({sd.first, sd.second, -1});
   }
   // Landing-slot assignment per receiver, in its program order: message m is
   // posted at the start of the compute before the Receive (post index =
   // computes seen - 1) and copied out at the start of its consumer compute.
   // A slot is reusable by a post at compute c once its occupant was copied
   // out at a compute <= c (the copy-out is enqueued before c's start event).
-  ipc_slots_.assign(P, 0);
+  plan.slots.assign(P, 0);
+  plan.post_order.assign(P, {});
   for (int p = 0; p < P; ++p) {
-    const auto& prog = list_.per_device[p];
+    const auto& prog = list.per_device[p];
     std::map<MsgKey, int> consumer;  // input key -> compute index of its consumer
     for (int i = 0, c = 0; i < static_cast<int>(prog.size()); ++i)
       if (prog[i].is_compute()) consumer[input_key(prog[i])] = c++;
     std::vector<int> free_at;  // slot -> compute index of its last copy-out
     int computes = 0;
     auto assign = [&](const MsgKey& k) {
-      const int post = computes - 1;
-      if (ipc_msgs_[ipc_index_.at(k)].src == rank_) ipc_send_order_[p].push_back(ipc_index_.at(k));
+      const int m = plan.index.at(k), post = computes - 1;
       auto cit = consumer.find(k);
       if (cit == consumer.end()) throw wavepipe::SimulationError("IPC transport: received message has no consumer");
       const int consume = cit->second;
@@ -71,9 +75,10 @@ void Runtime::ipc_setup() {
         free_at.push_back(consume);
       }
       free_at[slot] = consume;
-      ipc_msgs_[ipc_index_.at(k)].slot = slot;
+      plan.msgs[m].slot = slot;
+      plan.post_order[p].push_back(m);
     };
-    for (size_t i = 0; i < prog.size(); ++i) {
+    for (int i = 0; i < static_cast<int>(prog.size()); ++i) {
       const Action& a = prog[i];
       if (a.is_compute()) {
         ++computes;
@@ -81,20 +86,29 @@ void Runtime::ipc_setup() {
         assign(message_key(a));
       } else if (a.kind == ActionKind::BatchedExchange) {
         // the counterpart's outgoing message (ref include/wavepipe/action.hpp:67-73)
-        for (int q = 0; q < P; ++q)
-          for (const Action& b : list_.per_device[q])
-            if (b.kind == ActionKind::BatchedExchange && b.batch_group == a.batch_group && q != p)
-              assign(message_key(b));
+        for (const auto& [q, qi] : groups.at(a.batch_group))
+          if (q != p) assign(message_key(list.per_device[q][qi]));
       }
     }
-    ipc_slots_[p] = static_cast<int>(free_at.size());
+    plan.slots[p] = static_cast<int>(free_at.size());
   }
+  for (const auto& m : plan.msgs)
+    if (m.slot < 0) throw wavepipe::SimulationError("IPC transport: message without a receive");
+  return plan;
+}
+
+void Runtime::ipc_setup() {
+  const int P = list_.config.devices;
+  const IpcPlan plan = make_ipc_plan(list_);
+  ipc_index_ = plan.index;
+  for (const auto& m : plan.msgs) ipc_msgs_.push_back(IpcMsg{m.src, m.dst, m.slot, 0});
+  ipc_slots_ = plan.slots;
+  for (int p = 0; p < P; ++p)
+    for (int m : plan.post_order[p])
+      if (plan.msgs[m].src == rank_) ipc_send_order_[p].push_back(m);
   const size_t bytes = (message_bytes() + 255) & ~size_t(255);
   ipc_flag_bytes_ = ((2 * (ipc_msgs_.size() + replicas_) * sizeof(uint32_t)) + 4095) & ~size_t(4095);
-  for (IpcMsg& m : ipc_msgs_) {
-    if (m.slot < 0) throw wavepipe::SimulationError("IPC transport: message without a receive");
-    m.data_off = ipc_flag_bytes_ + size_t(m.slot) * bytes;
-  }
+  for (IpcMsg& m : ipc_msgs_) m.data_off = ipc_flag_bytes_ + size_t(m.slot) * bytes;
   ipc_arena_bytes_ = ipc_flag_bytes_ + size_t(ipc_slots_[rank_]) * bytes;
   DeviceState& d = *devs_[0];
   DevGuard g(d.cuda);

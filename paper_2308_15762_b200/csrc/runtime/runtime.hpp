@@ -79,6 +79,37 @@ struct MsgKey {
   }
 };
 
+// Message identity (payload, microbatch, lower slice of the boundary), the
+// reference's matching key (src/schedule.cpp:315-324, src/simulate.cpp:39-46).
+inline MsgKey message_key(const wavepipe::Action& a) {
+  const bool act = a.payload == static_cast<int>(wavepipe::Payload::Activation);
+  const bool out = a.kind == wavepipe::ActionKind::Send || a.kind == wavepipe::ActionKind::BatchedExchange;
+  return MsgKey{a.payload, a.microbatch,
+                act ? (out ? a.slice_index : a.slice_index - 1) : (out ? a.slice_index - 1 : a.slice_index)};
+}
+
+// The message a compute consumes: Forward of slice s takes the activation
+// of boundary s-1, Backward of slice s the gradient of boundary s.
+inline MsgKey input_key(const wavepipe::Action& a) {
+  return a.kind == wavepipe::ActionKind::Forward
+             ? MsgKey{static_cast<int>(wavepipe::Payload::Activation), a.microbatch, a.slice_index - 1}
+             : MsgKey{static_cast<int>(wavepipe::Payload::Gradient), a.microbatch, a.slice_index};
+}
+
+// Static plan of the CUDA-IPC transport, derived from the list alone (every
+// rank computes the same one; no GPU needed -- tested on CPU): the global
+// message table, each receiver's landing-slot assignment and post order.
+struct IpcPlan {
+  struct Msg {
+    int src, dst, slot;
+  };
+  std::map<MsgKey, int> index;
+  std::vector<Msg> msgs;
+  std::vector<int> slots;                    // device -> landing slots it needs
+  std::vector<std::vector<int>> post_order;  // device -> incoming message ids in its post order
+};
+IpcPlan make_ipc_plan(const wavepipe::ActionList& list);
+
 struct Published {
   int src = -1;
   BufPtr buf;
