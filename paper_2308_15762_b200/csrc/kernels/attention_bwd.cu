@@ -360,23 +360,26 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   }
 }
 
-// Delta[b, h, q] = sum_d dO * O over the head's D columns; warp per (row, head).
+// Delta[b, h, q] = sum_d dO * O over the head's D columns: D/8 lanes per
+// (token, head), one 16-byte load of each tensor per lane.
 __global__ void attn_bwd_prep_k(const __nv_bfloat16* dout, const __nv_bfloat16* out, float* delta, int T, int heads,
                                 int D, int seq, int hidden) {
-  const int wid = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (wid >= T * heads) return;
-  const int t = wid / heads, hd = wid % heads;
-  const __nv_bfloat16* a = dout + static_cast<int64_t>(t) * hidden + hd * D;
-  const __nv_bfloat16* o = out + static_cast<int64_t>(t) * hidden + hd * D;
+  const int lpr = D / 8;  // lanes per (token, head): 16 (D = 128) or 8 (D = 64)
+  const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / lpr, sub = threadIdx.x % lpr;
+  if (gid >= T * heads) return;
+  const int t = gid / heads, hd = gid % heads;
+  const int64_t off = static_cast<int64_t>(t) * hidden + hd * D + sub * 8;
+  const uint4 ua = *reinterpret_cast<const uint4*>(dout + off), uo = *reinterpret_cast<const uint4*>(out + off);
+  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&ua);
+  const __nv_bfloat162* o = reinterpret_cast<const __nv_bfloat162*>(&uo);
   float s = 0.f;
-  for (int c = lane * 2; c < D; c += 64) {
-    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + c));
-    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + c));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __bfloat1622float2(a[i]), y = __bfloat1622float2(o[i]);
     s += x.x * y.x + x.y * y.y;
   }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (lane == 0) {
+  for (int w = lpr / 2; w; w >>= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
+  if (sub == 0) {
     const int b = t / seq, q = t % seq;
     delta[(static_cast<int64_t>(b) * heads + hd) * seq + q] = s;
   }
@@ -450,8 +453,8 @@ int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const v
     throw std::runtime_error("flash_attn_bwd: needs seq % 128 == 0 and head_dim in {64, 128}");
   }
   const int T = s.mbs * s.seq;
-  const int warps = T * s.heads;
-  attn_bwd_prep_k<<<(warps + 7) / 8, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(dout),
+  const int64_t lanes = static_cast<int64_t>(T) * s.heads * (s.head_dim / 8);
+  attn_bwd_prep_k<<<static_cast<int>((lanes + 255) / 256), 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(dout),
                                                        static_cast<const __nv_bfloat16*>(out), delta, T, s.heads,
                                                        s.head_dim, s.seq, s.hidden);
   cudaMemsetAsync(dq_acc, 0, sizeof(float) * T * s.hidden, stream);
