@@ -42,6 +42,13 @@ sys.path.insert(0, ROOT)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 GPT13B = dict(layers=24, hidden=2048, heads=16, ffn=8192, seq=1024, vocab=50304)
+# BASELINE.json configs as presets (--model); the default is the headline one.
+MODELS = {
+    "gpt-1.3b-like": dict(GPT13B, causal=True),
+    "gpt2-medium-like": dict(layers=24, hidden=1024, heads=16, ffn=4096, seq=1024, vocab=50304, causal=True),
+    "bert-large-like": dict(layers=24, hidden=1024, heads=16, ffn=4096, seq=512, vocab=30528, causal=False),
+    "tiny-gpt": dict(layers=4, hidden=256, heads=4, ffn=1024, seq=128, vocab=1024, causal=True),
+}
 
 
 def load_peaks():
@@ -108,7 +115,8 @@ class ClockSampler:
 
 def model_desc(args):
     import paper_2308_15762_b200 as wp
-    return wp.ModelDesc(**GPT13B, micro_batch_size=args.mbs, causal=True, tie_embeddings=True, dtype="bf16",
+    m = MODELS[getattr(args, "model", "gpt-1.3b-like")]
+    return wp.ModelDesc(**m, micro_batch_size=args.mbs, tie_embeddings=True, dtype="bf16",
                         optimizer="adamw", lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.01, seed=1234)
 
 
@@ -173,7 +181,7 @@ def run_reference(args, rank, world):
     wall = time.perf_counter() - t0
     value = statistics.median(vals)
     ref_ms = ref_schedule_time(args.gpus, args.microbatches, args.waves)
-    sample = (f"1 sequence x (embedding + 1 of 24 layers + LM head) of GPT-1.3B, fp32 torch CPU "
+    sample = (f"1 sequence x (embedding + 1 of {desc.layers} layers + LM head) of {args.model}, fp32 torch CPU "
               f"fwd+bwd ({statistics.median(per):.2f} s), extrapolated to the full model by FLOPs; "
               f"schedule generate+simulate by the reference's own code (oracle/_ref): "
               f"{ref_ms if ref_ms is not None else 'n/a'} ms")
@@ -193,10 +201,12 @@ def workload_config(args, world):
     D = getattr(args, "replicas", 1)
     P = world // D
     par = f"pp{P}" + (f"xdp{D}" if D > 1 else "")
-    return {"workload": "GPT-1.3B-like train step, Hanayo W=%d over P=%d" % (args.waves, P)
+    name = getattr(args, "model", "gpt-1.3b-like")
+    m = MODELS[name]
+    return {"workload": "%s train step, Hanayo W=%d over P=%d" % (name, args.waves, P)
             + (f", {D} data-parallel replicas" if D > 1 else ""),
-            "model": "gpt-1.3b-like", "layers": 24, "hidden": 2048, "heads": 16, "ffn": 8192, "seq_len": 1024,
-            "vocab": 50304, "micro_batch_size": args.mbs, "microbatches": args.microbatches,
+            "model": name, "layers": m["layers"], "hidden": m["hidden"], "heads": m["heads"], "ffn": m["ffn"],
+            "seq_len": m["seq"], "vocab": m["vocab"], "micro_batch_size": args.mbs, "microbatches": args.microbatches,
             "global_batch": args.mbs * args.microbatches * D, "schedule": f"hanayo P={P} W={args.waves} "
             f"B={args.microbatches}" + (f" D={D}" if D > 1 else ""), "parallelism": par, "optimizer": "adamw",
             "l2_flush": "not needed: per-step working set (~35 GB) >> 126 MB L2"}
@@ -210,6 +220,8 @@ def main():
     ap.add_argument("--impl", default="wavepipe", choices=["wavepipe", "reference"])
     ap.add_argument("--microbatches", type=int, default=8)
     ap.add_argument("--mbs", type=int, default=16)
+    ap.add_argument("--model", default="gpt-1.3b-like", choices=sorted(MODELS),
+                    help="BASELINE.json config preset (default: the headline GPT-1.3B-like)")
     ap.add_argument("--waves", type=int, default=2)
     ap.add_argument("--replicas", type=int, default=1,
                     help="data-parallel replicas D (world = P*D ranks; IPC transport, peer-memory grad all-reduce)")
@@ -369,8 +381,8 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         v, dt, cores = cpu_port_sample(desc)
         cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
-               "sample": f"1 sequence x (embedding + 1 of 24 layers + LM head), fp32 torch CPU fwd+bwd "
-                         f"({dt:.2f} s), extrapolated to the 24-layer model by FLOPs"}
+               "sample": f"1 sequence x (embedding + 1 of {desc.layers} layers + LM head), fp32 torch CPU fwd+bwd "
+                         f"({dt:.2f} s), extrapolated to the {desc.layers}-layer model by FLOPs"}
     line = {
         "metric": "samples/sec (Hanayo W=2 train step)", "value": value, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
