@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   uint64_t* dq_full = bars + 8;
   uint64_t* dq_free = bars + 9;
   uint64_t* dkv_done = bars + 10;
+  uint64_t* dp_full = bars + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 4);
     mbar_init(dkv_done, 1);
+    mbar_init(dp_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -186,22 +188,25 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       const uint64_t dK = make_desc(aK, 16, 1024), dV = make_desc(aV, 16, 1024), dDS = make_desc(aDS, 16, 1024);
       const uint64_t dDSm = make_desc(aDS, ATOM, 1024), dKm = make_desc(aK, ATOM, 1024);
       mbar_wait(kv_full, 0);
-      for (int it = 0; it < n_it; ++it) {
+      // S^T(it) = K Q^T and dP^T(it) = V dO^T (reduction over D), committed
+      // separately: the softmax turns S into P while the previous tile's dQ
+      // is still being drained from the dP^T columns.
+      auto issue_s = [&](int it) {
         const int x = it & 1;
-        const uint32_t aQ = smem_u32(sQ + x * Cfg::TILE), aDO = smem_u32(sDO + x * Cfg::TILE);
-        const uint64_t dQ = make_desc(aQ, 16, 1024), dDO = make_desc(aDO, 16, 1024);
-        const uint64_t dDOm = make_desc(aDO, ATOM, 1024), dQm = make_desc(aQ, ATOM, 1024);
+        const uint64_t dQ = make_desc(smem_u32(sQ + x * Cfg::TILE), 16, 1024);
         mbar_wait(&qdo_full[x], (it >> 1) & 1);
         tc_fence_after();
-        // (S^T overwrites the P^T(it-1) columns: issued after dV(it-1), which read them.)
-        // S^T = K Q^T, dP^T = V dO^T (reduction over D)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * ATOM + (k & 3) * 32;
           tc_mma(tmem + kColS, desc_add(dK, off), desc_add(dQ, off), id_ss, k != 0);
         }
+        tc_commit(s_full);
+      };
+      auto issue_dp = [&](int it) {
+        const uint64_t dDO = make_desc(smem_u32(sDO + (it & 1) * Cfg::TILE), 16, 1024);
         if (it > 0) {
-          mbar_wait(dq_free, (it - 1) & 1);  // dQ_{it-1} drained from the dP columns
+          mbar_wait(dq_free, (it - 1) & 1);  // dQ(it-1) drained from the dP^T columns
           tc_fence_after();
         }
 #pragma unroll
@@ -209,7 +214,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           const uint32_t off = (k >> 2) * ATOM + (k & 3) * 32;
           tc_mma(tmem + kColDP, desc_add(dV, off), desc_add(dDO, off), id_ss, k != 0);
         }
-        tc_commit(s_full);
+        tc_commit(dp_full);
+      };
+      issue_s(0);
+      issue_dp(0);
+      for (int it = 0; it < n_it; ++it) {
+        const int x = it & 1;
+        const uint32_t aQ = smem_u32(sQ + x * Cfg::TILE), aDO = smem_u32(sDO + x * Cfg::TILE);
+        const uint64_t dDOm = make_desc(aDO, ATOM, 1024), dQm = make_desc(aQ, ATOM, 1024);
         mbar_wait(ds_full, it & 1);
         tc_fence_after();
         // dV += P^T dO (P^T from TMEM: queries [0,64) at columns 0.., [64,128) at 64..),
@@ -229,6 +241,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         }
         tc_commit(dq_full);
         tc_commit(pds_free);
+        if (it + 1 < n_it) {
+          issue_s(it + 1);   // overwrites the P^T(it) columns: in order after dV(it), which read them
+          issue_dp(it + 1);  // after the drain of dQ(it)
+        }
       }
       tc_commit(dkv_done);
     }
@@ -250,29 +266,40 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       named_bar(1, 256);
       mbar_wait(s_full, it & 1);
       tc_fence_after();
-      if (it > 0) mbar_wait(pds_free, (it - 1) & 1);
       const bool diag = p.causal && qi == kj;
-#pragma unroll 1
-      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 32) {
-        float s[32], dp[32];
-        tmem_ld32(tmem + lb + kColS + c0, s);
-        tmem_ld32(tmem + lb + kColDP + c0, dp);
-        float pv[32], ds[32];
+      // Phase A: P^T = 2^(s*scale - lse) from S^T alone; kept in registers
+      // for dS and written back over this half's S^T columns (bf16x2) as the
+      // A operand of dV += P^T dO.
+      float pv[64];
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int c0 = half * 64 + h2 * 32;
+        float sv[32];
+        tmem_ld32(tmem + lb + kColS + c0, sv);
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int c = c0 + i;
-          const float pr = (diag && c < r) ? 0.f : ex2f(s[i] * p.scale_log2 - lse[c]);
-          pv[i] = pr;
-          ds[i] = pr * (dp[i] - dl[c]) * p.scale;
+          pv[h2 * 32 + i] = (diag && c < r) ? 0.f : ex2f(sv[i] * p.scale_log2 - lse[c]);
         }
-        // P^T chunk -> bf16x2 -> TMEM over this half's own S^T columns (already read)
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          __nv_bfloat162 h = __floats2bfloat162_rn(pv[2 * i], pv[2 * i + 1]);
-          pk[i] = *reinterpret_cast<uint32_t*>(&h);
+          __nv_bfloat162 hh = __floats2bfloat162_rn(pv[h2 * 32 + 2 * i], pv[h2 * 32 + 2 * i + 1]);
+          pk[i] = *reinterpret_cast<uint32_t*>(&hh);
         }
-        tmem_st16(tmem + lb + kColS + half * 64 + (c0 - half * 64) / 2, pk);
+        tmem_st16(tmem + lb + kColS + half * 64 + h2 * 16, pk);
+      }
+      // Phase B: dS^T = P^T * (dP^T - Delta) / sqrt(D) once dP^T is in.
+      mbar_wait(dp_full, it & 1);
+      tc_fence_after();
+      if (it > 0) mbar_wait(pds_free, (it - 1) & 1);  // dS^T buffer free (dK, dQ, drain done)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int c0 = half * 64 + h2 * 32;
+        float dp[32], ds[32];
+        tmem_ld32(tmem + lb + kColDP + c0, dp);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) ds[i] = pv[h2 * 32 + i] * (dp[i] - dl[c0 + i]) * p.scale;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           uint4 ud;
