@@ -17,7 +17,7 @@ for _ in range(3):
     lib.wp_debug_flash_bwd(mbs,seq,heads,d,1,qkv.data_ptr(),ctx.data_ptr(),dout.data_ptr(),lse.data_ptr(),delta.data_ptr(),dq.data_ptr(),dqkv.data_ptr())
 buf=(C.c_ulonglong*512)()
 lib.wp_debug_bw_trace(buf,512)
-N={12:'sm_got_pdsfree',13:'dq_slabs_read',1:'mma_got_QdO',2:'mma_S_dP_committed',3:'mma_got_dS',4:'mma_dQ_committed',5:'sm_wait_S',6:'sm_got_S',7:'sm_dS_ready',8:'dq_wait',9:'dq_got',10:'dq_drained',11:'mma_got_dqfree'}
+N={12:'sm_wait_dP',13:'sm_got_dP',1:'mma_dP_committed',2:'mma_S_committed',3:'mma_got_dS',4:'mma_dQ_committed',5:'sm_wait_S',6:'sm_got_S',7:'sm_dS_ready',8:'dq_wait',9:'dq_got',10:'dq_drained',11:'mma_got_dqfree'}
 ev=sorted((buf[e*32+j],e,j) for e in range(16) for j in range(32) if buf[e*32+j])
 t0=ev[0][0]
 for t,e,j in ev: print(f"{t-t0:8d} it={j:2d} {N.get(e,e)}")
