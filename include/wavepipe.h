@@ -138,7 +138,7 @@ int wp_analytic_bubble_simplified(int devices, int waves, int64_t out[2]);
 /* ------------------------------------------------------------------------
  * GPU runtime: executes an ActionList on B200s (the reference's simulate()
  * replaced by real sm_100a kernels and NVLink transfers).  See
- * wavepipe/runtime.hpp for the C++ form `wavepipe::train_step`.
+ * include/wavepipe/runtime.hpp for the C++ form `wavepipe::train_step`.
  */
 
 /* ModelSpec: a GPT/BERT-like decoder stack.  dtype: 0 = fp32 (parity mode,
