@@ -50,7 +50,7 @@ template <int D>
 struct FaCfg {
   static constexpr int TILE = 128 * D * 2;  // one Q, K or V tile
   static constexpr int P_BYTES = QT * KT * 2;
-  static constexpr int SMEM = 2 * TILE + RING * TILE + 2 * P_BYTES + 1024 + 512;
+  static constexpr int SMEM = 2 * TILE + RING * TILE + 1024 + 512;  // P lives in TMEM
   __device__ static constexpr uint32_t col_s(int x) { return x ? 128u : 0u; }
   __device__ static constexpr uint32_t col_o(int x) { return x ? 256u + D : 256u; }
 };
@@ -118,6 +118,27 @@ __device__ unsigned long long g_fa_trace[16 * 2 * 32];
   } while (0)
 #endif
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+
+// O += P V with P read from tensor memory (A operand, K-major: lane = query,
+// 32-bit column j = keys 2j, 2j+1 as bf16x2) -- P never touches shared memory.
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -142,8 +163,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                     // [2] tiles
   uint8_t* sR = sQ + 2 * Cfg::TILE;       // [RING] K/V slots
-  uint8_t* sP = sR + RING * Cfg::TILE;    // [2] P tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * Cfg::P_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sR + RING * Cfg::TILE);
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;           // [RING]
   uint64_t* kv_empty = kv_full + RING;    // [RING]
@@ -193,7 +213,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (warp == 0 && lane == 0) {
       // ------------------------------------------------------------- TMA
       mbar_expect_tx(q_full, (has_b ? 2 : 1) * Cfg::TILE);
@@ -234,10 +254,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       auto free_tile = [&](int t) { tc_commit(&kv_empty[ring_slot(t)]); };
       auto issue_s = [&](int x, int j) {
         FA_TRACE(8, x, j);
-        if (j > 0) {
-          mbar_wait(&s_empty[x], (j - 1) & 1);  // the warpgroup has read S_x(j-1)
-          tc_fence_after();
-        }
+        // S_x(j) overwrites P_x(j-1): in order after PV_x(j-1), which read it.
         const uint32_t k_addr = tile_ready(2 * j);
         const uint32_t q_addr = smem_u32(sQ + x * Cfg::TILE);
         FA_TRACE(10, x, j);
@@ -255,13 +272,11 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         mbar_wait(&p_full[x], j & 1);
         tc_fence_after();
         const uint32_t v_addr = tile_ready(2 * j + 1);
-        const uint32_t p_addr = smem_u32(sP + x * Cfg::P_BYTES);
         FA_TRACE(11, x, j);
 #pragma unroll
         for (int k = 0; k < KT / 16; ++k) {
-          const uint64_t ad = make_desc(p_addr + (k >> 2) * ATOM + (k & 3) * 32, 16, 1024);
           const uint64_t bd = make_desc(v_addr + k * 2048, ATOM, 1024);
-          tc_mma(tmem + Cfg::col_o(x), ad, bd, idesc_pv, (j | k) != 0);
+          tc_mma_ts(tmem + Cfg::col_o(x), tmem + Cfg::col_s(x) + k * 8, bd, idesc_pv, (j | k) != 0);
         }
         tc_commit(&o_done[x]);
         FA_TRACE(2, x, j);
@@ -275,30 +290,22 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         issue_s(1, 0);
         free_tile(0);
       }
+      // Per step: PV_x(j) then S_x(j+1) for each warpgroup (S_x(j+1) reuses
+      // P_x(j)'s columns); the other warpgroup's softmax overlaps both.
       for (int j = 0; j < n_max; ++j) {
-        const bool a1 = j + 1 < nkv[0], b1 = j + 1 < nkv[1];
-        // Both next QK^T first (each only needs its warpgroup to have pulled
-        // S(j) into registers), then the two PVs as their P tiles land.
-        if (a1) {
-          issue_s(0, j + 1);
-          if (!b1) free_tile(2 * (j + 1));
-        }
-        if (b1) {
-          issue_s(1, j + 1);
-          free_tile(2 * (j + 1));
-        }
-        if (j < nkv[0]) {
-          issue_pv(0, j);
-          if (j >= nkv[1]) free_tile(2 * j + 1);
-        }
-        if (j < nkv[1]) {
-          issue_pv(1, j);
-          free_tile(2 * j + 1);
+        for (int x = 0; x < 2; ++x) {
+          if (j >= nkv[x]) continue;
+          issue_pv(x, j);
+          if (x == 1 || j >= nkv[1]) free_tile(2 * j + 1);
+          if (j + 1 < nkv[x]) {
+            issue_s(x, j + 1);
+            if (x == 1 || j + 1 >= nkv[1]) free_tile(2 * (j + 1));
+          }
         }
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
     // ---------------------------------------------------------- softmax
     const int x = (warp - 4) >> 2;  // 0: tile A, 1: tile B
     const int n_kv = nkv[x];
@@ -309,7 +316,6 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       const uint32_t lane_base = static_cast<uint32_t>(ew * 32) << 16;
       const uint32_t s_col = tmem + lane_base + Cfg::col_s(x);
       const uint32_t o_col = tmem + lane_base + Cfg::col_o(x);
-      uint8_t* myP = sP + x * Cfg::P_BYTES;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kv; ++j) {
         if (lane == 0 && (warp & 3) == 0) FA_TRACE(3, x, j);
@@ -320,9 +326,6 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         // for the next QK^T at once.
         float sv[KT];
         tmem_ld32x4(s_col, sv);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[x]);
         if (p.causal && j == qt[x]) {  // diagonal tile: keys after the query masked
 #pragma unroll
           for (int c = 0; c < KT; ++c) sv[c] = c > r ? -INFINITY : sv[c];
@@ -351,15 +354,18 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           tc_fence_after();
           if (lane == 0 && (warp & 3) == 0) FA_TRACE(6, x, j);
         }
-        // P row -> bf16 -> SW128 K-major smem (2 atoms of 64 keys).
+        // P row -> bf16x2 -> TMEM over this row's S columns (A operand of PV).
 #pragma unroll
-        for (int c = 0; c < KT / 8; ++c) {
-          uint4 u;
-          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+        for (int q = 0; q < KT / 32; ++q) {
+          uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(sv[8 * c + 2 * i], sv[8 * c + 2 * i + 1]);
-          *reinterpret_cast<uint4*>(myP + swz(r, c)) = u;
+          for (int i = 0; i < 16; ++i) {
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(sv[32 * q + 2 * i], sv[32 * q + 2 * i + 1]);
+            pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          tmem_st16(s_col + 16 * q, pk);
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         // Lazy rescale of O (before PV_x(j) is issued; S registers are dead).
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
@@ -371,7 +377,6 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             tmem_st32(o_col + c, o);
           }
         }
-        fence_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[x]);

@@ -58,7 +58,7 @@ def test_fp32_tiny_hanayo_p4_w2_b8():
     run_parity(desc, P=4, B=8, W=2)
 
 
-@pytest.mark.parametrize("P,B,W", [(1, 4, 1), (2, 4, 1), (2, 4, 3), (4, 4, 1), (3, 6, 2)])
+@pytest.mark.parametrize("P,B,W", [(1, 4, 1), (2, 4, 1), (2, 4, 3), (4, 4, 1), (3, 6, 2), (8, 8, 2), (4, 8, 4)])
 def test_fp32_schedules(P, B, W):
     desc = wp.ModelDesc(**dict(TINY, layers=2), dtype="fp32")
     run_parity(desc, P, B, W)
@@ -115,6 +115,23 @@ def test_bf16_parity():
     rt, params = build(desc, 2, 4, 2)
     rt.set_update(False)
     tokens, labels = synthetic_batch(4, desc.micro_batch_size, desc.seq, desc.vocab)
+    loss = rt.train_step(tokens, labels)
+    ref_loss, ref_grads = om.reference_step(params, tokens, labels, desc)
+    assert abs(loss - ref_loss) <= 1e-2 * abs(ref_loss)
+    for name, g in ref_grads.items():
+        e = rel(rt.get_grad(name, g.numel()), g.numpy())
+        assert e <= 5e-2, f"{name}: {e:.3g}"
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_bf16_parity_head_dim_64(causal):
+    """bf16 with 64-wide heads (the BERT-large / GPT2-medium head size) and
+    seq 256 through the fused attention; same stated tolerance."""
+    desc = wp.ModelDesc(layers=2, hidden=512, heads=8, ffn=2048, seq=256, vocab=2048, micro_batch_size=2,
+                        causal=causal, dtype="bf16")
+    rt, params = build(desc, 2, 4, 2)
+    rt.set_update(False)
+    tokens, labels = synthetic_batch(4, desc.micro_batch_size, desc.seq, desc.vocab, causal=causal)
     loss = rt.train_step(tokens, labels)
     ref_loss, ref_grads = om.reference_step(params, tokens, labels, desc)
     assert abs(loss - ref_loss) <= 1e-2 * abs(ref_loss)
