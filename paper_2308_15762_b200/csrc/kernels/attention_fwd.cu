@@ -36,14 +36,13 @@ constexpr int QT = 128;                 // queries per tile
 constexpr int KT = 128;                 // keys per tile
 constexpr int ATOM = 128 * 64 * 2;      // one SW128 K-major atom: 128 rows x 64 bf16 = 16 KB
 constexpr int FA_THREADS = 384;         // w0 TMA, w1 TMEM + MMA, w4-7 softmax A, w8-11 softmax B
-constexpr int RING = 3;                 // K/V tile slots: K_j in slot j%2, V_j in slot 2
+constexpr int NK = 2, NV = 2;           // K / V tile slots
+constexpr int RING = NK + NV;
 
-// Ring tile t: K_j = 2j, V_j = 2j+1.  K tiles alternate two slots (K_{j+1}
-// reuses K_{j-1}'s, free once both S(j-1) products are done -- early), V
-// tiles share the third (V_j reuses V_{j-1}'s, free at the end of step j-1,
-// and is needed only at the end of step j).
-__device__ __forceinline__ int ring_slot(int t) { return (t & 1) ? 2 : ((t >> 1) & 1); }
-__device__ __forceinline__ int ring_use(int t) { return (t & 1) ? (t >> 1) : (t >> 2); }
+// Ring tile t: K_j = 2j, V_j = 2j+1.  K tiles cycle NK slots, V tiles NV
+// slots (P lives in TMEM, so shared memory holds Q and NK + NV K/V tiles).
+__device__ __forceinline__ int ring_slot(int t) { return (t & 1) ? NK + (t >> 1) % NV : (t >> 1) % NK; }
+__device__ __forceinline__ int ring_use(int t) { return (t & 1) ? (t >> 1) / NV : (t >> 1) / NK; }
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 template <int D>
@@ -230,14 +229,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         for (int a = 0; a < D / 64; ++a)
           tma_load_4d(m, &kv_full[slot], sR + slot * Cfg::TILE + a * ATOM, a * 64, head, (t >> 1) * KT, b);
       };
-      // K_0, V_0, K_1, then K_{j+1} before V_j: each waits only for its own slot.
-      load(0);
-      load(1);
-      if (n_max > 1) load(2);
-      for (int j = 1; j < n_max; ++j) {
-        if (j + 1 < n_max) load(2 * (j + 1));
-        load(2 * j + 1);
-      }
+      // In consumption order: K_0, V_0, K_1, V_1, ... (S(j+1) is issued right
+      // after PV(j)); each load waits only for its own slot.
+      for (int t = 0; t < 2 * n_max; ++t) load(t);
     } else if (warp == 1 && lane == 0) {
       // ------------------------------------------------------------- MMA
       // S: M=128, N=128, A=Q K-major, B=K K-major.  PV: M=128, N=D, A=P K-major, B=V MN-major.
