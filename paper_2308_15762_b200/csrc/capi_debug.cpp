@@ -169,3 +169,28 @@ extern "C" int wp_debug_ipc_plan(const wp_list* list, int* slots, int* n_msgs, i
     return wpc::map_exception();
   }
 }
+
+#include "runtime/model.hpp"
+
+// The runtime's unit partition for a model and list (host only): bounds[S+1]
+// and per-unit forward costs (costs[n_units], n_units returned), for CPU tests.
+extern "C" int wp_debug_partition(const wp_model_desc* desc, const wp_list* list, int* bounds, double* costs,
+                                  int* n_units) {
+  try {
+    if (!desc || !list || !bounds || !n_units) return wpc::fail(WP_ERR_CONFIG, "null argument");
+    const auto m = wprt::ModelSpec::from_desc(*desc);
+    const auto units = wprt::build_units(m);
+    const auto& l = list->list;
+    std::vector<int> slice_device(l.config.stages, 0);
+    for (int d = 0; d < static_cast<int>(l.placement.assignment.size()); ++d)
+      for (const auto& sl : l.placement.assignment[d]) slice_device[sl.index] = d;
+    const auto b = wprt::partition_units(units, slice_device, l.config.devices);
+    for (size_t i = 0; i < b.size(); ++i) bounds[i] = b[i];
+    *n_units = static_cast<int>(units.size());
+    if (costs)
+      for (size_t i = 0; i < units.size(); ++i) costs[i] = units[i].cost;
+    return WP_OK;
+  } catch (...) {
+    return wpc::map_exception();
+  }
+}

@@ -104,7 +104,12 @@ Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, in
     throw wavepipe::ScheduleError("action list fails validation:\n" + wavepipe::render_diagnostics_text(rep));
   }
   units_ = build_units(m_);
-  bounds_ = partition_units(units_, list_.config.stages);
+  {
+    std::vector<int> slice_device(list_.config.stages, 0);
+    for (int d = 0; d < static_cast<int>(list_.placement.assignment.size()); ++d)
+      for (const auto& sl : list_.placement.assignment[d]) slice_device[sl.index] = d;
+    bounds_ = partition_units(units_, slice_device, list_.config.devices);
+  }
   const int P = list_.config.devices;
   if (m_.tie && owner_device(0, 0) != owner_device(0, list_.config.stages - 1)) {
     throw wavepipe::ConfigError(

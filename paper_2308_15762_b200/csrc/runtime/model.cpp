@@ -1,6 +1,7 @@
 #include "runtime/model.hpp"
 
 #include <cmath>
+#include <utility>
 #include <stdexcept>
 
 #include "wavepipe/core.hpp"
@@ -75,6 +76,75 @@ std::vector<int> partition_units(const std::vector<Unit>& units, int S) {
       }
     }
     b[k] = std::min(best, N - 1);
+  }
+  return b;
+}
+
+std::vector<int> partition_units(const std::vector<Unit>& units, const std::vector<int>& slice_device, int P) {
+  const int S = static_cast<int>(slice_device.size());
+  const int N = static_cast<int>(units.size());
+  std::vector<double> prefix(N + 1, 0.0);
+  for (int i = 0; i < N; ++i) prefix[i + 1] = prefix[i] + units[i].cost;
+  const double total = prefix[N];
+  // Per-slice targets: every device gets total / P; the pinned units (the
+  // embedding in slice 0, the LM head in slice S-1) count toward their
+  // device, whose other slices share what is left of its budget.
+  std::vector<double> fixed(S, 0.0), dev_fixed(P, 0.0);
+  std::vector<int> dev_slices(P, 0);
+  fixed[0] += units.front().cost;
+  fixed[S - 1] += units.back().cost;
+  for (int k = 0; k < S; ++k) {
+    dev_fixed[slice_device[k]] += fixed[k];
+    ++dev_slices[slice_device[k]];
+  }
+  std::vector<double> target(S);
+  double tsum = 0.0;
+  for (int k = 0; k < S; ++k) {
+    const int d = slice_device[k];
+    target[k] = fixed[k] + std::max(0.0, total / P - dev_fixed[d]) / dev_slices[d];
+    tsum += target[k];
+  }
+  std::vector<int> b(S + 1, 0);
+  b[S] = N;
+  double cum = 0.0;
+  for (int k = 1; k < S; ++k) {
+    cum += target[k - 1] * total / tsum;
+    int lo = std::max(b[k - 1], 1), best = lo;
+    double best_d = std::fabs(prefix[lo] - cum);
+    for (int i = lo + 1; i <= N - 1; ++i) {
+      const double dd = std::fabs(prefix[i] - cum);
+      if (dd < best_d) best = i, best_d = dd;
+    }
+    b[k] = std::min(best, N - 1);
+  }
+  // Coordinate descent on the cuts: each cut moves to the position that
+  // minimises (max device load, sum of squared device loads) until no cut
+  // moves.  Pipeline throughput is bounded by the busiest device.
+  auto score = [&](const std::vector<int>& bb) {
+    std::vector<double> load(P, 0.0);
+    for (int k = 0; k < S; ++k) load[slice_device[k]] += prefix[bb[k + 1]] - prefix[bb[k]];
+    double mx = 0.0, sq = 0.0;
+    for (double l : load) mx = std::max(mx, l), sq += l * l;
+    return std::make_pair(mx, sq);
+  };
+  auto cur = score(b);
+  for (bool moved = true; moved;) {
+    moved = false;
+    for (int k = 1; k < S; ++k) {
+      const int lo = std::max(b[k - 1], 1), hi = std::min(b[k + 1], N - 1);
+      int best = b[k];
+      auto best_s = cur;
+      for (int pos = lo; pos <= hi; ++pos) {
+        b[k] = pos;
+        const auto sc = score(b);
+        if (sc < best_s) best_s = sc, best = pos;
+      }
+      b[k] = best;
+      if (best_s < cur) {
+        cur = best_s;
+        moved = true;
+      }
+    }
   }
   return b;
 }

@@ -57,6 +57,14 @@ std::vector<Unit> build_units(const ModelSpec& m);
 // (identity) when S exceeds the unit count.
 std::vector<int> partition_units(const std::vector<Unit>& units, int S);
 
+// Device-balanced variant used by the runtime: slice k runs on pipeline
+// device slice_device[k] (the placement), and the cuts minimise the busiest
+// device's total cost (a synchronous flush step is bounded by it) rather
+// than equalising slices -- the LM head alone is ~2 layers of GPT-1.3B, so
+// equal slices leave the head's device (Hanayo device 0) 1.5x loaded at
+// P=8 W=2; balanced devices bring it to ~1.1x.
+std::vector<int> partition_units(const std::vector<Unit>& units, const std::vector<int>& slice_device, int P);
+
 // Parameters of one unit, in a fixed order (names are global, layer-indexed).
 std::vector<ParamDesc> unit_params(const ModelSpec& m, int unit_index, const Unit& u);
 
