@@ -85,11 +85,6 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {  // 16-B chunk c of row 
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
-               "f"(d)
-               : "memory");
-}
 
 template <int D>
 __global__ void __launch_bounds__(BW_THREADS, 1)
