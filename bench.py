@@ -312,6 +312,7 @@ def main():
     clk = clocks.stop()
     launches = rt.launch_count() - launches0
     g_launches, g_flops, g_sec = rt.gemm_stats()
+    a_launches, a_flops, a_sec = rt.attn_stats()
     if args.gemm_report and rank == 0:
         print(rt.gemm_report(), file=sys.stderr, flush=True)
     rt.set_profiling(False)
@@ -402,6 +403,10 @@ def main():
                      "traffic_launch": traffic_info,
                      "peak_kind": f"{peaks_kind} bf16 sustained (kernel timed inside a long step)",
                      "gemm_launches": g_launches, "gemm_share_of_step": g_sec / (sec * 1.0)},
+        "attention": {"kernel": "flash_fwd_kernel / flash_bwd_kernel (tcgen05)", "launches": a_launches,
+                      "achieved_tflops": a_flops / a_sec / 1e12 if a_sec > 0 else None,
+                      "frac_of_peak": a_flops / a_sec / 1e12 / peak_tc if a_sec > 0 else None,
+                      "share_of_step": a_sec / sec if sec > 0 else None},
         "cpu_baseline": cpu,
         "e2e": {"value": samples / sec_e2e, "unit": "samples/s",
                 "h2d_bytes_per_step": int(tok_h.numel() * 4 + lab_h.numel() * 4), "d2h_bytes_per_step": 4},

@@ -219,6 +219,9 @@ int wp_runtime_launch_count(const wp_runtime* rt, int64_t* launches);
  * own stream, accumulated over the steps run while enabled (enabling resets). */
 int wp_runtime_set_profiling(wp_runtime* rt, int enabled);
 int wp_runtime_gemm_stats(const wp_runtime* rt, int64_t* launches, double* flops, double* seconds);
+/* The same for the fused attention launches (algorithmic FLOPs: forward
+ * 4*mbs*heads*seq^2*d, halved when causal; backward 2.5x). */
+int wp_runtime_attn_stats(const wp_runtime* rt, int64_t* launches, double* flops, double* seconds);
 /* Text table of the profiled GEMMs by shape (launches, time, TFLOP/s). */
 int wp_runtime_gemm_report(const wp_runtime* rt, char* buf, int capacity);
 

@@ -109,6 +109,7 @@ _SIGS = {
     "wp_runtime_set_profiling": (I, [P, I]),
     "wp_runtime_gemm_stats": (I, [P, I64P, DP, DP]),
     "wp_runtime_gemm_report": (I, [P, C.c_char_p, I]),
+    "wp_runtime_attn_stats": (I, [P, I64P, DP, DP]),
 }
 
 EXPORTED = tuple(_SIGS)

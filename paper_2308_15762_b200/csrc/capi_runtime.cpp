@@ -65,6 +65,12 @@ int wp_runtime_ipc_connect(wp_runtime* rt, const void* handles, int nranks) {
   }
 }
 
+int wp_runtime_attn_stats(const wp_runtime* rt, int64_t* launches, double* flops, double* seconds) {
+  if (!rt || !launches || !flops || !seconds) return fail(WP_ERR_CONFIG, "null argument");
+  rt->rt->attn_stats(launches, flops, seconds);
+  return WP_OK;
+}
+
 int wp_runtime_memory(const wp_runtime* rt, int64_t* pool_bytes, int64_t* landing_bytes) {
   if (!rt || !pool_bytes || !landing_bytes) return fail(WP_ERR_CONFIG, "null argument");
   rt->rt->memory(pool_bytes, landing_bytes);

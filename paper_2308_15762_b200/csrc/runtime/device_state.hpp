@@ -91,6 +91,7 @@ struct DeviceState {
     double flops;
     cudaEvent_t s, e;
     std::string shape;
+    bool attention = false;  // fused attention launch (reported apart from the GEMMs)
   };
   std::vector<GemmRec> gemm_recs;
 };

@@ -591,6 +591,22 @@ void Runtime::gemm(DeviceState& d, const wpk::GemmProblem& g) {
   d.gemm_recs.push_back({2.0 * g.M * g.N * g.K * g.nb1 * g.nb2, s, e, shape});
 }
 
+template <typename F>
+void Runtime::timed_attention(DeviceState& d, bool backward, F&& launch) {
+  if (!profiling_) {
+    launch();
+    return;
+  }
+  cudaEvent_t s = next_event(d), e = next_event(d);
+  ck(cudaEventRecord(s, d.compute), "record attention start");
+  launch();
+  ck(cudaEventRecord(e, d.compute), "record attention end");
+  // algorithmic FLOPs: 4 mbs heads seq^2 d (half when causal); backward 2.5x
+  const double fwd = 4.0 * m_.mbs * m_.heads * double(m_.seq) * m_.seq * m_.head_dim() / (m_.causal ? 2.0 : 1.0);
+  d.gemm_recs.push_back({backward ? 2.5 * fwd : fwd, s, e, backward ? "flash attention bwd" : "flash attention fwd",
+                         true});
+}
+
 bool Runtime::use_flash() const {
   static const bool off = std::getenv("WP_NO_FLASH") != nullptr;
   return !off && m_.dtype == wpk::kBF16 && wpk::flash_supported(attn_shape());
@@ -661,7 +677,9 @@ BufPtr Runtime::unit_fwd(DeviceState& d, int ui, int mb, BufPtr x, UnitStash& st
       // Fused attention: ctx and the per-row log-sum-exp (the stash replaces P).
       st.b = f32(int64_t(m_.mbs) * H * S);
       st.c = act(int64_t(T) * h);
-      launches_ += wpk::flash_attn_fwd(attn_shape(), st.a->p, st.c->p, static_cast<float*>(st.b->p), cs);
+      timed_attention(d, false, [&] {
+        launches_ += wpk::flash_attn_fwd(attn_shape(), st.a->p, st.c->p, static_cast<float*>(st.b->p), cs);
+      });
     } else {
       // S = Q K^T / sqrt(d), per (head, sequence)
       wpk::GemmProblem sg;
@@ -820,8 +838,10 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   BufPtr dqkv;
   if (use_flash()) {
     dqkv = act(int64_t(T) * 3 * h);
-    launches_ += wpk::flash_attn_bwd(attn_shape(), st.a->p, st.c->p, dctx->p, static_cast<float*>(st.b->p),
-                                     d.attn_delta, d.dq_acc, dqkv->p, cs);
+    timed_attention(d, true, [&] {
+      launches_ += wpk::flash_attn_bwd(attn_shape(), st.a->p, st.c->p, dctx->p, static_cast<float*>(st.b->p),
+                                       d.attn_delta, d.dq_acc, dqkv->p, cs);
+    });
   } else {
     // dP = dctx V^T  (fp32 scratch)
     {
@@ -1133,9 +1153,15 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     for (const auto& r : d->gemm_recs) {
       float ms = 0.f;
       ck(cudaEventElapsedTime(&ms, r.s, r.e), "gemm time");
-      prof_seconds_ += 1e-3 * ms;
-      prof_flops_ += r.flops;
-      ++prof_launches_;
+      if (r.attention) {
+        attn_seconds_ += 1e-3 * ms;
+        attn_flops_ += r.flops;
+        ++attn_launches_;
+      } else {
+        prof_seconds_ += 1e-3 * ms;
+        prof_flops_ += r.flops;
+        ++prof_launches_;
+      }
       auto& st = prof_shapes_[r.shape];
       ++st.n;
       st.flops += r.flops;

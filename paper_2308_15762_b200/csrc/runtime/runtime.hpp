@@ -143,8 +143,14 @@ class Runtime {
     *flops = prof_flops_;
     *seconds = prof_seconds_;
   }
+  void attn_stats(int64_t* launches, double* flops, double* seconds) const {
+    *launches = attn_launches_;
+    *flops = attn_flops_;
+    *seconds = attn_seconds_;
+  }
   void reset_gemm_stats() {
     prof_launches_ = 0, prof_flops_ = 0, prof_seconds_ = 0;
+    attn_launches_ = 0, attn_flops_ = 0, attn_seconds_ = 0;
     prof_shapes_.clear();
   }
   // Per GEMM shape: "MxNxK b<batch> <A,B majorness> c<causal>" -> (launches, flops, seconds).
@@ -208,8 +214,11 @@ class Runtime {
   std::vector<std::string> param_names_;
   std::map<MsgKey, Published> published_;
   bool tracing_ = false, update_ = true, profiling_ = false;
-  int64_t prof_launches_ = 0;
-  double prof_flops_ = 0, prof_seconds_ = 0;
+  int64_t prof_launches_ = 0, attn_launches_ = 0;
+  double prof_flops_ = 0, prof_seconds_ = 0, attn_flops_ = 0, attn_seconds_ = 0;
+  // Profiling of one fused-attention launch (fwd or bwd) on the compute stream.
+  template <typename F>
+  void timed_attention(DeviceState& d, bool backward, F&& launch);
   struct ShapeStat {
     int64_t n = 0;
     double flops = 0, seconds = 0;

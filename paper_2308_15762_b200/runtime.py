@@ -172,6 +172,13 @@ class Runtime:
         check(lib.wp_runtime_gemm_stats(self._h, C.byref(n), C.byref(fl), C.byref(sec)))
         return n.value, fl.value, sec.value
 
+    def attn_stats(self):
+        """(launches, algorithmic FLOPs, summed kernel seconds) of the fused
+        attention launches run while profiling was enabled."""
+        n, fl, sec = C.c_int64(), C.c_double(), C.c_double()
+        check(lib.wp_runtime_attn_stats(self._h, C.byref(n), C.byref(fl), C.byref(sec)))
+        return n.value, fl.value, sec.value
+
     def gemm_report(self):
         buf = C.create_string_buffer(1 << 16)
         check(lib.wp_runtime_gemm_report(self._h, buf, len(buf)))
