@@ -260,12 +260,28 @@ def main():
     cfg = wp.make_config(wp.Scheme.Hanayo, P, args.microbatches, args.waves, D)
     sched = wp.generate_schedule(cfg)
     transport = os.environ.get("WP_TRANSPORT", "ipc")
-    if world > 1 and transport == "nccl" and D == 1:
+
+    def nccl_runtime():
         obj = [wp.runtime.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_NCCL, device_ids=[dev], rank=rank, nccl_id=obj[0])
+        return wp.Runtime(desc, sched, transport=wp.TRANSPORT_NCCL, device_ids=[dev], rank=rank, nccl_id=obj[0])
+
+    if world > 1 and transport == "nccl" and D == 1:
+        rt = nccl_runtime()
     elif world > 1:
         rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_IPC, device_ids=[dev], rank=rank)
+        ok, why = rt.ipc_status()
+        flag = torch.tensor([1 if ok else 0], device="cpu" if share else "cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            # an unsupported peer path on this box: every rank switches together
+            if not ok:
+                print(f"rank {rank}: IPC transport probe failed ({why}); falling back to NCCL", file=sys.stderr)
+            if D > 1:
+                raise SystemExit("data-parallel replicas need the IPC transport")
+            rt.close()
+            transport = "nccl"
+            rt = nccl_runtime()
     else:
         rt = wp.Runtime(desc, sched, device_ids=[dev])
 

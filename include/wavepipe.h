@@ -185,6 +185,10 @@ void wp_runtime_free(wp_runtime* rt);
 #define WP_IPC_HANDLE_BYTES 128
 int wp_runtime_ipc_handle(wp_runtime* rt, void* out);
 int wp_runtime_ipc_connect(wp_runtime* rt, const void* handles, int nranks);
+/* After connect: *ok = 1 if every mapped peer accepted a probe copy and a
+ * stream-memory-op write (the step's operations); else 0 and the reason in
+ * `msg`, so all ranks can agree on another transport before stepping. */
+int wp_runtime_ipc_status(const wp_runtime* rt, int* ok, char* msg, int capacity);
 /* ncclGetUniqueId for rank 0 of a WP_TRANSPORT_NCCL job (128 bytes). */
 int wp_nccl_unique_id(void* out128);
 

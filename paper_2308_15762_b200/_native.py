@@ -95,6 +95,7 @@ _SIGS = {
     "wp_nccl_unique_id": (I, [C.c_void_p]),
     "wp_runtime_ipc_handle": (I, [P, C.c_void_p]),
     "wp_runtime_ipc_connect": (I, [P, C.c_void_p, I]),
+    "wp_runtime_ipc_status": (I, [P, IP, C.c_char_p, I]),
     "wp_train_step": (I, [P, C.c_void_p, C.c_void_p, I, C.POINTER(C.c_float)]),
     "wp_runtime_trace": (I, [P, PP]),
     "wp_runtime_set_tracing": (I, [P, I]),

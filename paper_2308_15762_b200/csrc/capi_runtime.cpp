@@ -77,6 +77,18 @@ int wp_runtime_memory(const wp_runtime* rt, int64_t* pool_bytes, int64_t* landin
   return WP_OK;
 }
 
+int wp_runtime_ipc_status(const wp_runtime* rt, int* ok, char* msg, int capacity) {
+  if (!rt || !ok) return fail(WP_ERR_CONFIG, "null argument");
+  *ok = rt->rt->ipc_ok() ? 1 : 0;
+  if (msg && capacity > 0) {
+    const std::string& e = rt->rt->ipc_error();
+    const size_t n = std::min<size_t>(e.size(), size_t(capacity) - 1);
+    std::memcpy(msg, e.data(), n);
+    msg[n] = 0;
+  }
+  return WP_OK;
+}
+
 int wp_nccl_unique_id(void* out128) {
   if (!out128) return fail(WP_ERR_CONFIG, "null argument");
   ncclUniqueId id;

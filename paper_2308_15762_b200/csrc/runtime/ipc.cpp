@@ -107,7 +107,9 @@ void Runtime::ipc_setup() {
     for (int m : plan.post_order[p])
       if (plan.msgs[m].src == rank_) ipc_send_order_[p].push_back(m);
   const size_t bytes = (message_bytes() + 255) & ~size_t(255);
-  ipc_flag_bytes_ = ((2 * (ipc_msgs_.size() + replicas_) * sizeof(uint32_t)) + 4095) & ~size_t(4095);
+  // flags: arrive[M], posted[M], ready[D], done[D], then one probe word per global rank
+  ipc_flag_bytes_ =
+      ((2 * (ipc_msgs_.size() + replicas_) + size_t(P) * replicas_) * sizeof(uint32_t) + 4095) & ~size_t(4095);
   for (IpcMsg& m : ipc_msgs_) m.data_off = ipc_flag_bytes_ + size_t(m.slot) * bytes;
   ipc_arena_bytes_ = ipc_flag_bytes_ + size_t(ipc_slots_[rank_]) * bytes;
   DeviceState& d = *devs_[0];
@@ -175,6 +177,26 @@ void Runtime::ipc_connect(const void* handles, int nranks) {
        "dp table");
   }
   ipc_connected_ = true;
+  // Probe every mapped peer once with the operations the steps use -- a
+  // copy-engine write and a stream-memory-op write into its arena (this
+  // rank's own probe word) -- so an unsupported peer path fails here, at
+  // set-up, where every rank can agree on a fallback, instead of mid-step.
+  try {
+    DeviceState& d = *devs_[0];
+    const size_t probe = (2 * (ipc_msgs_.size() + replicas_) + size_t(grank(replica_, rank_))) * sizeof(uint32_t);
+    for (char* peer : ipc_peer_) {
+      if (!peer) continue;
+      ck(cudaMemcpyAsync(peer + probe, ipc_arena_ + probe, sizeof(uint32_t), cudaMemcpyDeviceToDevice, d.sig),
+         "IPC probe copy");
+      StreamOps::write(d.sig, reinterpret_cast<uint32_t*>(peer + probe), 0u);
+    }
+    ck(cudaStreamSynchronize(d.sig), "IPC probe");
+    ipc_ok_ = true;
+  } catch (const std::exception& e) {
+    ipc_ok_ = false;
+    ipc_error_ = e.what();
+    cudaGetLastError();
+  }
 }
 
 void Runtime::ipc_release() {

@@ -166,6 +166,9 @@ class Runtime {
   // cudaIpcMemHandle_t), then map every peer's from the handles of all ranks.
   void ipc_handle(void* out64) const;
   void ipc_connect(const void* handles, int nranks);
+  // Result of the set-up probe of every mapped peer (copy + stream-op write).
+  bool ipc_ok() const { return ipc_ok_; }
+  const std::string& ipc_error() const { return ipc_error_; }
   // Bytes of one inter-stage message (activation or input-gradient).
   size_t message_bytes() const { return size_t(m_.tokens()) * m_.hidden * m_.act_bytes(); }
   void get_param(const std::string& name, float* host, int64_t n, bool grad);
@@ -265,7 +268,8 @@ class Runtime {
   char* ipc_arena_ = nullptr;
   size_t ipc_flag_bytes_ = 0, ipc_arena_bytes_ = 0;
   std::vector<char*> ipc_peer_;  // global rank -> mapped arena (nullptr: not a peer)
-  bool ipc_connected_ = false;
+  bool ipc_connected_ = false, ipc_ok_ = false;
+  std::string ipc_error_;
   uint32_t epoch_ = 0;
   // Data-parallel replicas (list config D > 1, IPC transport only): global
   // rank = replica * P + pipeline device.  The arena's flag region also holds

@@ -114,6 +114,13 @@ class Runtime:
             allh = C.create_string_buffer(b"".join(blobs), world * IPC_HANDLE_BYTES)
             check(lib.wp_runtime_ipc_connect(self._h, allh, world))
 
+    def ipc_status(self):
+        """(ok, message) of the IPC transport's set-up probe of its peers."""
+        ok = C.c_int()
+        msg = C.create_string_buffer(512)
+        check(lib.wp_runtime_ipc_status(self._h, C.byref(ok), msg, len(msg)))
+        return bool(ok.value), msg.value.decode()
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             lib.wp_runtime_free(self._h)

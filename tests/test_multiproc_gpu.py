@@ -75,6 +75,8 @@ def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q, D=1):
         P = world // D
         sched = wp.generate_schedule(wp.make_config(wp.Scheme.Hanayo, P, B, W, D))
         rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_IPC, device_ids=[dev], rank=rank)
+        ok, why = rt.ipc_status()
+        assert ok, why  # the set-up probe of every mapped peer (copy + stream-op write)
         params = om.init_params(desc, seed=21)
         replica = rank // P
         losses, grads = _run(rt, params, B, desc, steps, update, replica=replica)
