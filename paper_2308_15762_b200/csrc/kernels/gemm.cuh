@@ -50,6 +50,18 @@ struct Epilogue {
   // bias gradient of the layer whose input gradient C is).  Fused into the
   // CTA-pair kernel's epilogue; other paths add a column-sum pass.
   float* colsum = nullptr;
+  // Optional, CTA-pair kernel with a bf16 C only: LayerNorm-backward partials
+  // of C = dLN for the LN whose input is ln_x (same dtype / ld as C):
+  //   ln_dw[n] += sum_m C * xhat,   colsum (set it to ln_db) += sum_m C,
+  //   ln_rows[2m] += sum_n C * ln_w[n],  ln_rows[2m+1] += sum_n C * ln_w[n] * xhat,
+  // xhat = (ln_x - ln_mean[m]) * ln_rstd[m] -- the LN's dw / db and the two row
+  // sums its dx needs, so dx becomes an elementwise pass (layernorm_bwd_dx_rows).
+  const void* ln_x = nullptr;
+  const float* ln_mean = nullptr;
+  const float* ln_rstd = nullptr;
+  const float* ln_w = nullptr;
+  float* ln_dw = nullptr;
+  float* ln_rows = nullptr;
 };
 
 // Causal structure inside each batch element (an s x s attention block,

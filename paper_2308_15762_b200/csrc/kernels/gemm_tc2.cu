@@ -57,15 +57,22 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
   constexpr int dt = CPC == 32 ? kF32 : kBF16;
   const bool needs_in = mode == kEpiResidual || mode == kEpiDGelu;
   uint8_t* sb = slabs + buf * SLAB_BYTES;
+  const bool ln = CPC == 64 && e.ln_x != nullptr;  // LayerNorm-backward partials (store mode, bf16 C)
+  const int xb = buf ^ 1;                          // the LN input slab (buf flips below)
+  uint8_t* sx = slabs + xb * SLAB_BYTES;
   if (lane == 0) {
     // the slab(s) about to be written must have been read out by earlier stores
-    if (mode == kEpiGelu) bulk_wait_read<0>();
+    if (mode == kEpiGelu || ln) bulk_wait_read<0>();
     else bulk_wait_read<1>();
   }
   __syncwarp();
   if (needs_in && lane == 0) {
     mbar_expect_tx(&sbar[buf], SLAB_BYTES);
     tma_load_2d(map_x, &sbar[buf], sb, gcol, row0);
+  }
+  if (ln && lane == 0) {
+    mbar_expect_tx(&sbar[xb], SLAB_BYTES);
+    tma_load_2d(map_x, &sbar[xb], sx, gcol, row0);
   }
   float v[CPC];
   tmem_ld32(taddr, v);
@@ -131,6 +138,48 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
       bulk_commit();
     }
     buf ^= 1;
+  }
+  if (ln) {
+    // LayerNorm-backward partials of this slab (v = dLN, still intact):
+    // per-row sums of g = dLN * w and g * xhat, and dw's column sums of
+    // dLN * xhat (db is the colsum below).
+    mbar_wait(&sbar[xb], (sphase >> xb) & 1);
+    sphase ^= 1u << xb;
+    float xv[CPC];
+    slab_get_bf16(sx, lane, xv);
+    const int row = row0 + lane;
+    const bool valid = row < p.M;
+    const float mu = valid ? e.ln_mean[row] : 0.f, rs = valid ? e.ln_rstd[row] : 0.f;
+    float sg = 0.f, sgx = 0.f;
+#pragma unroll
+    for (int i = 0; i < CPC; ++i) {
+      const float wv = gcol + i < p.N ? e.ln_w[gcol + i] : 0.f;
+      const float xh = (xv[i] - mu) * rs;
+      const float g = v[i] * wv;
+      sg += g;
+      sgx += g * xh;
+      xv[i] = valid ? v[i] * xh : 0.f;  // dw term
+    }
+    if (valid) {
+      atomicAdd(e.ln_rows + 2 * row, sg);
+      atomicAdd(e.ln_rows + 2 * row + 1, sgx);
+    }
+#pragma unroll
+    for (int q = 0; q < CPC / 32; ++q) {
+      float* w = xv + 32 * q;
+#pragma unroll
+      for (int sh = 16; sh >= 1; sh >>= 1) {
+        const bool up = (lane & sh) != 0;
+#pragma unroll
+        for (int i = 0; i < sh; ++i) {
+          const float send = up ? w[i] : w[i + sh];
+          const float keep = up ? w[i + sh] : w[i];
+          w[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+        }
+      }
+      const int col = gcol + 32 * q + lane;
+      if (col < p.N) atomicAdd(e.ln_dw + col, w[0]);
+    }
   }
   if (e.colsum) {
     // Column sums of this slab's 32 rows (one per lane): a transposing
@@ -363,7 +412,9 @@ void launch_pair(const GemmProblem& g, const Params& p, cudaStream_t s) {
     const Epilogue& e = g.epi;
     const int dt = e.mode == kEpiAccum ? kF32 : e.c_dtype;
     mc = make_slab_map(e.c, dt, g.N, g.M, e.ldc);
-    const void* x = e.mode == kEpiResidual ? e.resid : (e.mode == kEpiGelu || e.mode == kEpiDGelu) ? e.aux : nullptr;
+    const void* x = e.mode == kEpiResidual ? e.resid
+                    : (e.mode == kEpiGelu || e.mode == kEpiDGelu) ? e.aux
+                                                                  : e.ln_x;
     mx = x ? make_slab_map(x, dt, g.N, g.M, e.ldc) : mc;
   }
   const int pairs = std::min(p.num_tiles * std::max(1, p.k_split), num_sms() / 2);
@@ -379,6 +430,9 @@ int gemm_tc2(const GemmProblem& g, cudaStream_t s) {
   p.group_m = std::max(1, std::min(gm_env, p.tiles_m));
   static const bool te_off = std::getenv("WP_GEMM_NO_TMA_EPI") != nullptr;  // A/B switch for profiling
   const bool te = p.vec_ok && !te_off;
+  if (g.epi.ln_x && (!te || g.epi.mode != kEpiStore || g.epi.c_dtype != kBF16)) {
+    throw std::runtime_error("gemm: LayerNorm-backward partials need the TMA epilogue, store mode and a bf16 C");
+  }
   // Split-K for the fp32 gradient accumulation (the TMA reduce-add epilogue
   // makes partial tiles commutative): a 2-way split when it fills the last
   // wave of SM pairs better (measured: deeper splits and ranges shorter than

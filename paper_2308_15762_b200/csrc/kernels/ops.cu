@@ -334,6 +334,32 @@ __global__ void __launch_bounds__(512, 1) ln_bwd_cols_k(const T* dy, const T* x,
     }
 }
 
+// Elementwise LayerNorm dx from precomputed row sums (see ops.cuh): 8
+// contiguous elements per thread, 16-byte accesses, grid-stride.
+template <typename T>
+__global__ void __launch_bounds__(256) ln_bwd_dx_rows_k(const T* dy, const T* x, const float* mean,
+                                                        const float* rstd, const float* w, const float* rows,
+                                                        const T* dres, T* dx, int64_t n8, int h) {
+  const float inv_h = 1.f / h;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t off = i * 8;
+    const int row = static_cast<int>(off / h), col = static_cast<int>(off % h);
+    float d[8], xv[8], wv[8], r[8], o[8];
+    load8(dy + off, d);
+    load8(x + off, xv);
+    load8(w + col, wv);
+    if (dres) load8(dres + off, r);
+    const float mu = mean[row], rs = rstd[row], sg = rows[2 * row] * inv_h, sgx = rows[2 * row + 1] * inv_h;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float xh = (xv[k] - mu) * rs;
+      o[k] = rs * (d[k] * wv[k] - sg - xh * sgx) + (dres ? r[k] : 0.f);
+    }
+    store8(dx + off, o);
+  }
+}
+
 // dw, db: lane <-> column (coalesced), 8 warps stride over a row range, block
 // partials reduced in shared memory, one atomic per column per block.
 template <typename T>
@@ -790,6 +816,24 @@ int layernorm_bwd(int dtype, const void* dy, const void* x, const float* mean, c
                                  static_cast<const bf16*>(dres), static_cast<bf16*>(dx), dw, db, T_, h, s);
   return ln_bwd_dispatch<float>(static_cast<const float*>(dy), static_cast<const float*>(x), mean, rstd, w,
                                 static_cast<const float*>(dres), static_cast<float*>(dx), dw, db, T_, h, s);
+}
+
+int layernorm_bwd_dx_rows(int dtype, const void* dy, const void* x, const float* mean, const float* rstd,
+                          const float* w, const float* rows, const void* dres, void* dx, int T_, int h,
+                          cudaStream_t s) {
+  if (h % 8) throw std::runtime_error("layernorm_bwd_dx_rows: hidden must be a multiple of 8");
+  const int64_t n8 = static_cast<int64_t>(T_) * h / 8;
+  const int grid = static_cast<int>(std::min<int64_t>((n8 + 255) / 256, 8 * sm_count()));
+  if (dtype == kBF16)
+    ln_bwd_dx_rows_k<bf16><<<grid, 256, 0, s>>>(static_cast<const bf16*>(dy), static_cast<const bf16*>(x), mean,
+                                                rstd, w, rows, static_cast<const bf16*>(dres), static_cast<bf16*>(dx),
+                                                n8, h);
+  else
+    ln_bwd_dx_rows_k<float><<<grid, 256, 0, s>>>(static_cast<const float*>(dy), static_cast<const float*>(x), mean,
+                                                 rstd, w, rows, static_cast<const float*>(dres),
+                                                 static_cast<float*>(dx), n8, h);
+  check_launch("layernorm_bwd_dx_rows");
+  return 1;
 }
 
 int softmax_fwd(int dtype, const float* S, void* P, int rows, int n, int causal, cudaStream_t s) {

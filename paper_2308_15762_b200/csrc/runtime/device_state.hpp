@@ -50,6 +50,7 @@ struct DeviceState {
   float* scores = nullptr;  // fp32 [mbs, heads, seq, seq] scratch (unfused attention)
   float* attn_delta = nullptr;  // fp32 [mbs, heads, seq] (fused attention backward)
   float* dq_acc = nullptr;      // fp32 [T, h]             (fused attention backward)
+  float* ln_rows = nullptr;     // fp32 [T, 2]  LayerNorm-backward row sums (GEMM-fused path)
   std::vector<std::pair<int, int>> be_partner;  // per position: (device, position) of a BE's counterpart
 
   // per-step program state

@@ -202,7 +202,8 @@ Runtime::~Runtime() {
     for (void* p : {static_cast<void*>(d->master), static_cast<void*>(d->grad), static_cast<void*>(d->m),
                     static_cast<void*>(d->v), d->shadow, static_cast<void*>(d->loss), static_cast<void*>(d->tokens),
                     static_cast<void*>(d->labels), static_cast<void*>(d->scores),
-                    static_cast<void*>(d->attn_delta), static_cast<void*>(d->dq_acc)})
+                    static_cast<void*>(d->attn_delta), static_cast<void*>(d->dq_acc),
+                    static_cast<void*>(d->ln_rows)})
       if (p) cudaFree(p);
     d->pool.reset();
     if (d->compute) cudaStreamDestroy(d->compute);
@@ -276,6 +277,7 @@ void Runtime::build_devices(const int* device_ids) {
     ck(cudaMalloc(&d->loss, sizeof(float)), "cudaMalloc loss");
     ck(cudaMalloc(&d->tokens, sizeof(int32_t) * B * T), "cudaMalloc tokens");
     ck(cudaMalloc(&d->labels, sizeof(int32_t) * B * T), "cudaMalloc labels");
+    ck(cudaMalloc(&d->ln_rows, sizeof(float) * 2 * size_t(T)), "cudaMalloc ln rows");
     if (use_flash()) {
       ck(cudaMalloc(&d->attn_delta, sizeof(float) * size_t(m_.mbs) * m_.heads * m_.seq), "cudaMalloc delta");
       ck(cudaMalloc(&d->dq_acc, sizeof(float) * size_t(T) * m_.hidden), "cudaMalloc dq");
@@ -767,8 +769,15 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     return nullptr;
   }
   // dX = dY W  (B N-major: W[k][n] with k = out features)
+  // LayerNorm-backward fused into the dgrad GEMM producing dLN (bf16, the
+  // CTA-pair kernel's shapes): the epilogue accumulates dw, db and the two
+  // row sums, leaving dx to an elementwise pass.  WP_LN_UNFUSED=1 keeps the
+  // standalone kernel (A/B switch).
+  static const bool ln_unfused = std::getenv("WP_LN_UNFUSED") != nullptr;
+  const bool ln_fused = !ln_unfused && dt == wpk::kBF16 && T >= 256 && h > 128 && h % 8 == 0 &&
+                        std::getenv("WP_GEMM_NO_PAIR") == nullptr && std::getenv("WP_GEMM_NO_TMA_EPI") == nullptr;
   auto dgrad = [&](const void* dY, int ld_dy, int n_out, const void* W, int n_in, void* dX, int mode = wpk::kEpiStore,
-                   const void* aux = nullptr, float* colsum = nullptr) {
+                   const void* aux = nullptr, float* colsum = nullptr, const std::string& ln_name = std::string()) {
     wpk::GemmProblem g;
     g.in_dtype = dt;
     g.M = T, g.N = n_in, g.K = n_out;
@@ -776,6 +785,12 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     g.B = op(W, n_in, true);
     g.epi.mode = mode, g.epi.c = dX, g.epi.c_dtype = dt, g.epi.ldc = n_in, g.epi.aux = const_cast<void*>(aux);
     g.epi.colsum = colsum;
+    if (ln_fused && !ln_name.empty()) {
+      ck(cudaMemsetAsync(d.ln_rows, 0, sizeof(float) * 2 * size_t(T), cs), "ln rows reset");
+      g.epi.ln_x = st.x->p, g.epi.ln_mean = static_cast<float*>(st.mean->p);
+      g.epi.ln_rstd = static_cast<float*>(st.rstd->p), g.epi.ln_w = master(d, ln_name + ".w");
+      g.epi.ln_dw = grad(d, ln_name + ".w"), g.epi.colsum = grad(d, ln_name + ".b"), g.epi.ln_rows = d.ln_rows;
+    }
     gemm(d, g);
   };
   // dW += dY^T X  (both operands MN-major over the token dimension)
@@ -790,6 +805,12 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   };
   auto ln_bwd = [&](const BufPtr& dln, const std::string& name, const BufPtr& dres) {
     BufPtr dx = act(int64_t(T) * h);
+    if (ln_fused) {  // dw, db, row sums came with dLN from the dgrad GEMM
+      launches_ += wpk::layernorm_bwd_dx_rows(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p),
+                                              static_cast<float*>(st.rstd->p), master(d, name + ".w"), d.ln_rows,
+                                              dres ? dres->p : nullptr, dx->p, T, h, cs);
+      return dx;
+    }
     LnBwdCheck chk;
     if (check_ops_enabled())
       chk.before(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p), static_cast<float*>(st.rstd->p),
@@ -806,7 +827,7 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   if (u.kind == UnitKind::Head) {
     const std::string wn = m_.tie ? "wte" : "lm_head.w";
     BufPtr dln = act(int64_t(T) * h);
-    dgrad(st.a->p, V, V, weight(d, wn), h, dln->p);
+    dgrad(st.a->p, V, V, weight(d, wn), h, dln->p, wpk::kEpiStore, nullptr, nullptr, "lnf");
     wgrad(st.a->p, V, st.ln->p, h, grad(d, wn));
     BufPtr dx = ln_bwd(dln, "lnf", nullptr);
     drop(dln);
@@ -822,7 +843,7 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "mlp.fc2.b"), T, h, h, cs);
     wgrad(du->p, f, st.ln->p, h, grad(d, L + "mlp.fc1.w"));
     BufPtr dln = act(int64_t(T) * h);
-    dgrad(du->p, f, f, weight(d, L + "mlp.fc1.w"), h, dln->p);
+    dgrad(du->p, f, f, weight(d, L + "mlp.fc1.w"), h, dln->p, wpk::kEpiStore, nullptr, nullptr, L + "ln2");
     BufPtr dx = ln_bwd(dln, L + "ln2", dy);
     drop(du);
     drop(dln);
@@ -898,7 +919,7 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   wgrad(dqkv->p, 3 * h, st.ln->p, h, grad(d, L + "attn.qkv.w"));
   launches_ += wpk::colsum_accum(dt, dqkv->p, grad(d, L + "attn.qkv.b"), T, 3 * h, 3 * h, cs);
   BufPtr dln = act(int64_t(T) * h);
-  dgrad(dqkv->p, 3 * h, 3 * h, weight(d, L + "attn.qkv.w"), h, dln->p);
+  dgrad(dqkv->p, 3 * h, 3 * h, weight(d, L + "attn.qkv.w"), h, dln->p, wpk::kEpiStore, nullptr, nullptr, L + "ln1");
   BufPtr dx = ln_bwd(dln, L + "ln1", dy);
   drop(dctx);
   drop(dqkv);
