@@ -64,7 +64,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
 }
 
 struct BwParams {
-  int seq, heads, n_tiles, causal, hidden;
+  int batch, seq, heads, n_tiles, causal, hidden;
   float scale_log2, scale;
   const float* lse2;
   const float* delta;
@@ -115,9 +115,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kj = static_cast<int>(blockIdx.x % p.n_tiles);  // light-to-heavy order reversed: small kj = most q tiles
-  const int head = static_cast<int>((blockIdx.x / p.n_tiles) % p.heads);
-  const int b = static_cast<int>(blockIdx.x / (p.n_tiles * p.heads));
+  // Heaviest-first (LPT) order: all (batch, head) CTAs of key tile 0 -- the
+  // most causal query tiles -- launch before those of tile 1, and so on.
+  const int bh = p.batch * p.heads;
+  const int kj = static_cast<int>(blockIdx.x / bh);
+  const int head = static_cast<int>(blockIdx.x % bh % p.heads);
+  const int b = static_cast<int>(blockIdx.x % bh / p.heads);
   const int i0 = p.causal ? kj : 0;
   const int n_it = p.n_tiles - i0;
 
@@ -449,6 +452,7 @@ void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const flo
   const CUtensorMap mq = bw_map(base, s, ld), mk = bw_map(base + s.hidden, s, ld),
                     mv = bw_map(base + 2 * s.hidden, s, ld), mdo = bw_map(dout, s, s.hidden);
   BwParams p;
+  p.batch = s.mbs;
   p.seq = s.seq;
   p.heads = s.heads;
   p.n_tiles = s.seq / T128;

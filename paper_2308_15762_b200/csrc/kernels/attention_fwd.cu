@@ -55,7 +55,7 @@ struct FaCfg {
 };
 
 struct FaParams {
-  int seq, heads, n_q_tiles, n_pairs, causal;
+  int batch, seq, heads, n_q_tiles, n_pairs, causal;
   float scale_log2;
   __nv_bfloat16* ctx;
   int ld_ctx;
@@ -174,9 +174,12 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // Heavy (late) query-tile pairs first for causal load balance.
-  const int pi = p.n_pairs - 1 - static_cast<int>(blockIdx.x % p.n_pairs);
-  const int head = static_cast<int>((blockIdx.x / p.n_pairs) % p.heads);
-  const int b = static_cast<int>(blockIdx.x / (p.n_pairs * p.heads));
+  // Heaviest-first (LPT) order: the last query-tile pair (longest causal key
+  // range) of every (batch, head) launches first.
+  const int bh = p.batch * p.heads;
+  const int pi = p.n_pairs - 1 - static_cast<int>(blockIdx.x / bh);
+  const int head = static_cast<int>(blockIdx.x % bh % p.heads);
+  const int b = static_cast<int>(blockIdx.x % bh / p.heads);
   const int qt[2] = {2 * pi, 2 * pi + 1};
   const bool has_b = qt[1] < p.n_q_tiles;
   const int n_all = p.seq / KT;
@@ -435,6 +438,7 @@ void launch_fwd(const AttnShape& s, const void* qkv, void* ctx, float* lse2, cud
   const auto* base = static_cast<const __nv_bfloat16*>(qkv);
   const CUtensorMap mq = attn_map(base, s), mk = attn_map(base + s.hidden, s), mv = attn_map(base + 2 * s.hidden, s);
   FaParams p;
+  p.batch = s.mbs;
   p.seq = s.seq;
   p.heads = s.heads;
   p.n_q_tiles = s.seq / QT;
