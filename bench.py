@@ -319,22 +319,30 @@ def main():
     for _ in range(args.warmup):
         rt.train_step(tok_d, lab_d)
 
-    # Device-resident timed region (value), with GEMM profiling and clocks.
-    rt.set_profiling(True)
+    # Device-resident timed region (value), with clocks sampled during it.
     launches0 = rt.launch_count()
     clocks = ClockSampler(dev)
     clocks.start()
     sec, loss = timed(args.steps, host=False)
     clk = clocks.stop()
     launches = rt.launch_count() - launches0
+
+    # End-to-end through the public API from pinned host buffers.
+    sec_e2e, _ = timed(args.steps, host=True)
+
+    # Per-kernel-class device time (roofline / attention objects) from a
+    # separate profiled pass: the per-launch events it records would
+    # otherwise slow the timed region above.
+    rt.set_profiling(True)
+    prof_steps = max(2, args.steps // 2)
+    sec_prof, _ = timed(prof_steps, host=False)
     g_launches, g_flops, g_sec = rt.gemm_stats()
     a_launches, a_flops, a_sec = rt.attn_stats()
     if args.gemm_report and rank == 0:
         print(rt.gemm_report(), file=sys.stderr, flush=True)
     rt.set_profiling(False)
-
-    # End-to-end through the public API from pinned host buffers.
-    sec_e2e, _ = timed(args.steps, host=True)
+    g_launches //= prof_steps
+    a_launches //= prof_steps
 
     # One traced step: measured vs simulated bubble.  Each rank traces its
     # own pipeline device relative to its step start (right after a
@@ -418,11 +426,11 @@ def main():
                      "frac": achieved / peak_tc if achieved else None, "traffic": traffic,
                      "traffic_launch": traffic_info,
                      "peak_kind": f"{peaks_kind} bf16 sustained (kernel timed inside a long step)",
-                     "gemm_launches": g_launches, "gemm_share_of_step": g_sec / (sec * 1.0)},
+                     "gemm_launches": g_launches, "gemm_share_of_step": g_sec / sec_prof},
         "attention": {"kernel": "flash_fwd_kernel / flash_bwd_kernel (tcgen05)", "launches": a_launches,
                       "achieved_tflops": a_flops / a_sec / 1e12 if a_sec > 0 else None,
                       "frac_of_peak": a_flops / a_sec / 1e12 / peak_tc if a_sec > 0 else None,
-                      "share_of_step": a_sec / sec if sec > 0 else None},
+                      "share_of_step": a_sec / sec_prof if sec_prof > 0 else None},
         "cpu_baseline": cpu,
         "e2e": {"value": samples / sec_e2e, "unit": "samples/s",
                 "h2d_bytes_per_step": int(tok_h.numel() * 4 + lab_h.numel() * 4), "d2h_bytes_per_step": 4},
