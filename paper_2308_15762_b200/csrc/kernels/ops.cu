@@ -752,11 +752,11 @@ int ln_bwd_dispatch(const T* dy, const T* x, const float* mean, const float* rst
   return 2;
 }
 
-// One-shot all-reduce (mean) of this replica's share; float4 granules, fixed
-// summation order (replica 0..D-1) so every replica stores the same bits.
-constexpr int kMaxReplicas = 16;
-__global__ void allreduce_mean_k(float* const* bufs, int D, int64_t lo4, int64_t hi4, float scale) {
-  float4* b[kMaxReplicas];
+// One-shot all-reduce (scaled sum) of this member's share; float4 granules,
+// fixed summation order (member 0..G-1) so every member stores the same bits.
+constexpr int kMaxGroup = 32;
+__global__ void allreduce_scaled_k(float* const* bufs, int D, int64_t lo4, int64_t hi4, float scale) {
+  float4* b[kMaxGroup];
   for (int r = 0; r < D; ++r) b[r] = reinterpret_cast<float4*>(bufs[r]);
   for (int64_t i = lo4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < hi4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -854,15 +854,15 @@ int softmax_bwd(int dtype, const float* dP, void* P, int rows, int n, float scal
   return 1;
 }
 
-int allreduce_mean_peers(float* const* bufs, int D, int me, int64_t n, cudaStream_t s) {
-  if (D < 1 || D > kMaxReplicas) throw std::runtime_error("allreduce: 1 <= replicas <= 16");
+int allreduce_scaled_peers(float* const* bufs, int D, int me, int64_t n, float scale, cudaStream_t s) {
+  if (D < 1 || D > kMaxGroup) throw std::runtime_error("allreduce: 1 <= group size <= 32");
   if (n % 4) throw std::runtime_error("allreduce: length must be a multiple of 4");
   const int64_t n4 = n / 4, per = (n4 + D - 1) / D;
   const int64_t lo = std::min(n4, per * me), hi = std::min(n4, lo + per);
   if (hi <= lo) return 0;
   const int grid = static_cast<int>(std::min<int64_t>(4 * sm_count(), (hi - lo + 255) / 256));
-  allreduce_mean_k<<<grid, 256, 0, s>>>(bufs, D, lo, hi, 1.0f / D);
-  check_launch("allreduce_mean_peers");
+  allreduce_scaled_k<<<grid, 256, 0, s>>>(bufs, D, lo, hi, scale);
+  check_launch("allreduce_scaled_peers");
   return 1;
 }
 

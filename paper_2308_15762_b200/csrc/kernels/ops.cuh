@@ -57,11 +57,12 @@ struct OptimArgs {
 int optimizer_step(const OptimArgs& a, float* master, float* grad, float* m, float* v, void* shadow_bf16, int64_t n,
                    cudaStream_t s);
 
-// Data-parallel gradient all-reduce over peer memory: bufs[0..D) are the D
-// replicas' fp32 gradient buffers (NVLink-mapped; bufs[me] local).  Replica
-// `me` owns elements [me*n/D, (me+1)*n/D) (float4 granules): it sums them over
-// all D buffers, scales by 1/D and stores the mean into every buffer.
-int allreduce_mean_peers(float* const* bufs, int D, int me, int64_t n, cudaStream_t s);
+// Gradient all-reduce over peer memory: bufs[0..G) are the group's fp32
+// gradient buffers (NVLink-mapped; bufs[me] local).  Member `me` owns
+// elements [me*n/G, (me+1)*n/G) (float4 granules): it sums them over all G
+// buffers, multiplies by `scale` (1/D for D data-parallel replicas) and
+// stores the result into every buffer.
+int allreduce_scaled_peers(float* const* bufs, int G, int me, int64_t n, float scale, cudaStream_t s);
 
 // Deterministic N(0, std) init from a counter-based hash (Box-Muller).
 int init_normal(float* p, int64_t n, float std, uint64_t seed, cudaStream_t s);

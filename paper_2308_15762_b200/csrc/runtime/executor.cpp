@@ -48,13 +48,24 @@ Pool::~Pool() {
 BufPtr Pool::alloc(size_t bytes, cudaStream_t stream, int cls) {
   bytes = (bytes + 255) & ~size_t(255);
   auto& fl = free_[{cls, bytes}];
-  if (!fl.empty()) {
-    BufPtr b = fl.back();
-    fl.pop_back();
-    if (b->ev_pending) {
-      ck(cudaStreamWaitEvent(stream, b->ev, 0), "pool wait");
-      b->ev_pending = false;
+  // Reuse a buffer only if that adds no wait on another stream's pending
+  // work: a message buffer freed by a push on a copy stream is busy until
+  // the receiver posts it, and making the compute stream wait for that
+  // would turn the reference's buffered sends (src/simulate.cpp:117-122)
+  // into blocking ones -- a cross-device wait the action list does not have
+  // (it deadlocks Chimera P=4).  Such buffers are skipped and the pool grows
+  // by the messages in flight instead.
+  for (size_t i = fl.size(); i-- > 0;) {
+    BufPtr b = fl[i];
+    if (b->ev_pending && b->released_on != stream) {
+      const cudaError_t q = cudaEventQuery(b->ev);
+      if (q == cudaErrorNotReady) continue;
+      ck(q, "pool event query");
+    } else if (b->ev_pending) {
+      ck(cudaStreamWaitEvent(stream, b->ev, 0), "pool wait");  // same stream: program order, no new wait
     }
+    b->ev_pending = false;
+    fl.erase(fl.begin() + static_cast<long>(i));
     return b;
   }
   DevGuard g(dev_);
@@ -79,6 +90,7 @@ void Pool::release(const BufPtr& b, cudaStream_t stream) {
     }
     ck(cudaEventRecord(b->ev, stream), "pool release record");
     b->ev_pending = true;
+    b->released_on = stream;
   }
   free_[{b->pool_class, b->bytes}].push_back(b);
 }
@@ -111,9 +123,20 @@ Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, in
     bounds_ = partition_units(units_, slice_device, list_.config.devices);
   }
   const int P = list_.config.devices;
-  if (m_.tie && owner_device(0, 0) != owner_device(0, list_.config.stages - 1)) {
+  if (m_.tie) {  // every device holding the embedding slice also holds the head slice (Hanayo, Chimera)
+    for (const auto& dev : list_.placement.assignment) {
+      bool first = false, last = false;
+      for (const auto& sl : dev) first |= sl.index == 0, last |= sl.index == list_.config.stages - 1;
+      if (first != last) {
+        throw wavepipe::ConfigError(
+            "tie_embeddings needs the first and last slice on one device (true for Hanayo and Chimera placements)");
+      }
+    }
+  }
+  if (list_.config.scheme == wavepipe::Scheme::Chimera && transport_ != WP_TRANSPORT_IPC) {
     throw wavepipe::ConfigError(
-        "tie_embeddings needs the first and last slice on one device (true for Hanayo placements)");
+        "Chimera holds every stage on two devices (p and P-1-p) that sum their gradients over peer memory: "
+        "it needs the IPC transport (one process per device)");
   }
   if (transport_ != WP_TRANSPORT_LOCAL && transport_ != WP_TRANSPORT_NCCL && transport_ != WP_TRANSPORT_IPC) {
     throw wavepipe::ConfigError("unknown transport");
@@ -997,7 +1020,7 @@ void Runtime::backward(DeviceState& d, const Action& a) {
 }
 
 void Runtime::optimizer(DeviceState& d) {
-  if (replicas_ > 1) dp_allreduce(d);
+  if (grad_group_.size() > 1) dp_allreduce(d);
   if (!update_) return;
   wpk::OptimArgs o{m_.optimizer, m_.lr, m_.beta1, m_.beta2, m_.eps, m_.weight_decay, step_ + 1};
   launches_ += wpk::optimizer_step(o, d.master, d.grad, d.m, d.v, d.shadow, d.nparam, d.compute);

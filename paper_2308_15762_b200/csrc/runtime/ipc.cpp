@@ -24,6 +24,7 @@
 //       M = messages of the list, D = data-parallel replicas;
 //       arrive[m] is used when r receives m, posted[m] when r sends m
 //   [ landing slots of r ]
+#include <algorithm>
 #include <cstring>
 
 #include "runtime/device_state.hpp"
@@ -54,13 +55,14 @@ IpcPlan make_ipc_plan(const wavepipe::ActionList& list) {
   // A slot is reusable by a post at compute c once its occupant was copied
   // out at a compute <= c (the copy-out is enqueued before c's start event).
   plan.slots.assign(P, 0);
-  plan.post_order.assign(P, {});
+  plan.issue_order.assign(P, {});
   for (int p = 0; p < P; ++p) {
     const auto& prog = list.per_device[p];
     std::map<MsgKey, int> consumer;  // input key -> compute index of its consumer
     for (int i = 0, c = 0; i < static_cast<int>(prog.size()); ++i)
       if (prog[i].is_compute()) consumer[input_key(prog[i])] = c++;
     std::vector<int> free_at;  // slot -> compute index of its last copy-out
+    std::vector<std::pair<int, int>> by_consumer;  // (consumer compute, message)
     int computes = 0;
     auto assign = [&](const MsgKey& k) {
       const int m = plan.index.at(k), post = computes - 1;
@@ -76,7 +78,7 @@ IpcPlan make_ipc_plan(const wavepipe::ActionList& list) {
       }
       free_at[slot] = consume;
       plan.msgs[m].slot = slot;
-      plan.post_order[p].push_back(m);
+      by_consumer.push_back({consume, m});
     };
     for (int i = 0; i < static_cast<int>(prog.size()); ++i) {
       const Action& a = prog[i];
@@ -91,6 +93,17 @@ IpcPlan make_ipc_plan(const wavepipe::ActionList& list) {
       }
     }
     plan.slots[p] = static_cast<int>(free_at.size());
+    // Pushes to p go out in the order p consumes them.  A per-peer copy
+    // stream is FIFO, so a push waits for every earlier one to that peer;
+    // in consumer order those earlier messages are ones p needs before this
+    // one anyway (each compute has one input), so the FIFO adds no wait the
+    // list itself does not have and cannot deadlock a list the reference's
+    // simulator runs (src/simulate.cpp:123-133).  Post order is not enough:
+    // an exchange's incoming half can be posted early and consumed late
+    // (Chimera), and a later-posted, earlier-consumed message would queue
+    // behind it.
+    std::sort(by_consumer.begin(), by_consumer.end());
+    for (const auto& cm : by_consumer) plan.issue_order[p].push_back(cm.second);
   }
   for (const auto& m : plan.msgs)
     if (m.slot < 0) throw wavepipe::SimulationError("IPC transport: message without a receive");
@@ -104,12 +117,21 @@ void Runtime::ipc_setup() {
   for (const auto& m : plan.msgs) ipc_msgs_.push_back(IpcMsg{m.src, m.dst, m.slot, 0});
   ipc_slots_ = plan.slots;
   for (int p = 0; p < P; ++p)
-    for (int m : plan.post_order[p])
+    for (int m : plan.issue_order[p])
       if (plan.msgs[m].src == rank_) ipc_send_order_[p].push_back(m);
   const size_t bytes = (message_bytes() + 255) & ~size_t(255);
-  // flags: arrive[M], posted[M], ready[D], done[D], then one probe word per global rank
-  ipc_flag_bytes_ =
-      ((2 * (ipc_msgs_.size() + replicas_) + size_t(P) * replicas_) * sizeof(uint32_t) + 4095) & ~size_t(4095);
+  grad_group_.clear();
+  for (int r = 0; r < replicas_; ++r) {
+    grad_group_.push_back(grank(r, rank_));
+    if (chimera_mirror() != rank_) grad_group_.push_back(grank(r, chimera_mirror()));
+  }
+  std::sort(grad_group_.begin(), grad_group_.end());
+  group_me_ = static_cast<int>(std::find(grad_group_.begin(), grad_group_.end(), grank(replica_, rank_)) -
+                               grad_group_.begin());
+  grad_scale_ = 1.f / static_cast<float>(replicas_);
+  const size_t G = grad_group_.size();
+  // flags: arrive[M], posted[M], ready[G], done[G], then one probe word per global rank
+  ipc_flag_bytes_ = ((2 * (ipc_msgs_.size() + G) + size_t(P) * replicas_) * sizeof(uint32_t) + 4095) & ~size_t(4095);
   for (IpcMsg& m : ipc_msgs_) m.data_off = ipc_flag_bytes_ + size_t(m.slot) * bytes;
   ipc_arena_bytes_ = ipc_flag_bytes_ + size_t(ipc_slots_[rank_]) * bytes;
   DeviceState& d = *devs_[0];
@@ -128,8 +150,8 @@ void Runtime::ipc_setup() {
   }
   ck(cudaStreamCreateWithFlags(&d.sig, cudaStreamNonBlocking), "stream");
   ipc_peer_.assign(size_t(P) * replicas_, nullptr);
-  dp_grads_.assign(replicas_, nullptr);
-  dp_grads_[replica_] = d.grad;
+  dp_grads_.assign(G, nullptr);
+  dp_grads_[group_me_] = d.grad;
 }
 
 void Runtime::ipc_handle(void* out64) const {
@@ -165,15 +187,17 @@ void Runtime::ipc_connect(const void* handles, int nranks) {
   }
   for (int q = 0; q < list_.config.devices; ++q)
     if (peer[q] && q != rank_) ipc_peer_[grank(replica_, q)] = static_cast<char*>(open(grank(replica_, q), 0));
-  // The same pipeline device in every other replica: flags and gradients.
-  for (int r = 0; r < replicas_; ++r) {
-    if (r == replica_) continue;
-    ipc_peer_[grank(r, rank_)] = static_cast<char*>(open(grank(r, rank_), 0));
-    dp_grads_[r] = static_cast<float*>(open(grank(r, rank_), 1));
+  // The gradient group (same device in every other replica, Chimera mirror):
+  // flags and gradients.
+  for (int g = 0; g < static_cast<int>(grad_group_.size()); ++g) {
+    if (g == group_me_) continue;
+    const int q = grad_group_[g];
+    if (!ipc_peer_[q]) ipc_peer_[q] = static_cast<char*>(open(q, 0));
+    dp_grads_[g] = static_cast<float*>(open(q, 1));
   }
-  if (replicas_ > 1) {
-    ck(cudaMalloc(&dp_grads_dev_, sizeof(float*) * replicas_), "cudaMalloc dp table");
-    ck(cudaMemcpy(dp_grads_dev_, dp_grads_.data(), sizeof(float*) * replicas_, cudaMemcpyHostToDevice),
+  if (grad_group_.size() > 1) {
+    ck(cudaMalloc(&dp_grads_dev_, sizeof(float*) * grad_group_.size()), "cudaMalloc dp table");
+    ck(cudaMemcpy(dp_grads_dev_, dp_grads_.data(), sizeof(float*) * grad_group_.size(), cudaMemcpyHostToDevice),
        "dp table");
   }
   ipc_connected_ = true;
@@ -183,7 +207,8 @@ void Runtime::ipc_connect(const void* handles, int nranks) {
   // set-up, where every rank can agree on a fallback, instead of mid-step.
   try {
     DeviceState& d = *devs_[0];
-    const size_t probe = (2 * (ipc_msgs_.size() + replicas_) + size_t(grank(replica_, rank_))) * sizeof(uint32_t);
+    const size_t probe =
+        (2 * (ipc_msgs_.size() + grad_group_.size()) + size_t(grank(replica_, rank_))) * sizeof(uint32_t);
     for (char* peer : ipc_peer_) {
       if (!peer) continue;
       ck(cudaMemcpyAsync(peer + probe, ipc_arena_ + probe, sizeof(uint32_t), cudaMemcpyDeviceToDevice, d.sig),
@@ -207,8 +232,8 @@ void Runtime::ipc_release() {
     if (p) cudaIpcCloseMemHandle(p);
     p = nullptr;
   }
-  for (int r = 0; r < static_cast<int>(dp_grads_.size()); ++r)
-    if (r != replica_ && dp_grads_[r]) cudaIpcCloseMemHandle(dp_grads_[r]);
+  for (int g = 0; g < static_cast<int>(dp_grads_.size()); ++g)
+    if (g != group_me_ && dp_grads_[g]) cudaIpcCloseMemHandle(dp_grads_[g]);
   dp_grads_.clear();
   if (dp_grads_dev_) cudaFree(dp_grads_dev_);
   dp_grads_dev_ = nullptr;
@@ -220,7 +245,7 @@ void Runtime::ipc_release() {
 
 // Send / outgoing half of an exchange: the message is ready once its
 // producer's event is recorded; it is issued (ipc_flush) in the receiver's
-// post order.  Nothing here blocks the sender's compute stream.
+// consumer order.  Nothing here blocks the sender's compute stream.
 void Runtime::ipc_send(DeviceState& d, const Action& a) {
   const MsgKey out = message_key(a);
   auto it = d.outbox.find(out);
@@ -232,7 +257,7 @@ void Runtime::ipc_send(DeviceState& d, const Action& a) {
   ipc_flush(d, ipc_msgs_[m].dst);
 }
 
-// Issue every ready message to `peer` that is next in its post order: the
+// Issue every ready message to `peer` that is next in its consumer order: the
 // per-peer copy stream waits for the producer (ready event) and for the
 // receiver's post, pushes the bytes into the peer's landing slot, then raises
 // the peer's arrival flag to this step's epoch.
@@ -301,23 +326,26 @@ void Runtime::ipc_land(DeviceState& d, const Action& a) {
   }
 }
 
-// Gradient all-reduce across the D replicas of this pipeline device, on the
-// compute stream right before the optimizer (the flush): publish "my grads
-// are final" to every replica, wait for theirs, run one peer-memory kernel
-// in which each replica averages its 1/D share over all D buffers (NVLink
-// loads) and writes the mean back into all of them (NVLink stores), then
-// publish / wait "done" so no buffer is reused while a peer still reads it.
+// Gradient all-reduce across this rank's gradient group (the D replicas of
+// its pipeline device; for Chimera also their mirrors P-1-p, which hold the
+// same stages for the opposite direction), on the compute stream right
+// before the optimizer (the flush): publish "my grads are final" to every
+// member, wait for theirs, run one peer-memory kernel in which each member
+// sums its 1/G share over all G buffers (NVLink loads), scales by 1/D and
+// writes the result back into all of them (NVLink stores), then publish /
+// wait "done" so no buffer is reused while a peer still reads it.
 void Runtime::dp_allreduce(DeviceState& d) {
   cudaStream_t s = d.compute;
-  for (int r = 0; r < replicas_; ++r)
-    if (r != replica_) StreamOps::write(s, ipc_dp_flag(ipc_peer_[grank(r, rank_)], 0, replica_), epoch_);
-  for (int r = 0; r < replicas_; ++r)
-    if (r != replica_) StreamOps::wait_geq(s, ipc_dp_flag(ipc_arena_, 0, r), epoch_);
-  launches_ += wpk::allreduce_mean_peers(dp_grads_dev_, replicas_, replica_, d.nparam, s);
-  for (int r = 0; r < replicas_; ++r)
-    if (r != replica_) StreamOps::write(s, ipc_dp_flag(ipc_peer_[grank(r, rank_)], 1, replica_), epoch_);
-  for (int r = 0; r < replicas_; ++r)
-    if (r != replica_) StreamOps::wait_geq(s, ipc_dp_flag(ipc_arena_, 1, r), epoch_);
+  const int G = static_cast<int>(grad_group_.size());
+  for (int g = 0; g < G; ++g)
+    if (g != group_me_) StreamOps::write(s, ipc_dp_flag(ipc_peer_[grad_group_[g]], 0, group_me_), epoch_);
+  for (int g = 0; g < G; ++g)
+    if (g != group_me_) StreamOps::wait_geq(s, ipc_dp_flag(ipc_arena_, 0, g), epoch_);
+  launches_ += wpk::allreduce_scaled_peers(dp_grads_dev_, G, group_me_, d.nparam, grad_scale_, s);
+  for (int g = 0; g < G; ++g)
+    if (g != group_me_) StreamOps::write(s, ipc_dp_flag(ipc_peer_[grad_group_[g]], 1, group_me_), epoch_);
+  for (int g = 0; g < G; ++g)
+    if (g != group_me_) StreamOps::wait_geq(s, ipc_dp_flag(ipc_arena_, 1, g), epoch_);
 }
 
 }  // namespace wprt

@@ -44,6 +44,7 @@ struct Buf {
   int pool_class = 0;  // 0 compute-only, 1 message
   cudaEvent_t ev = nullptr;
   bool ev_pending = false;
+  cudaStream_t released_on = nullptr;
 };
 using BufPtr = std::shared_ptr<Buf>;
 
@@ -98,7 +99,7 @@ inline MsgKey input_key(const wavepipe::Action& a) {
 
 // Static plan of the CUDA-IPC transport, derived from the list alone (every
 // rank computes the same one; no GPU needed -- tested on CPU): the global
-// message table, each receiver's landing-slot assignment and post order.
+// message table, each receiver's landing-slot assignment and push issue order.
 struct IpcPlan {
   struct Msg {
     int src, dst, slot;
@@ -106,7 +107,9 @@ struct IpcPlan {
   std::map<MsgKey, int> index;
   std::vector<Msg> msgs;
   std::vector<int> slots;                    // device -> landing slots it needs
-  std::vector<std::vector<int>> post_order;  // device -> incoming message ids in its post order
+  // device -> incoming message ids in the order of their consumer computes:
+  // the order every sender issues its pushes to that device (see ipc.cpp)
+  std::vector<std::vector<int>> issue_order;
 };
 IpcPlan make_ipc_plan(const wavepipe::ActionList& list);
 
@@ -259,7 +262,7 @@ class Runtime {
   // program order), so a copy waiting for its post never holds up a message
   // the peer needs first; the host defers a produced message until every
   // message the peer posts earlier has been issued.
-  std::map<int, std::vector<int>> ipc_send_order_;  // peer -> message ids in the peer's post order
+  std::map<int, std::vector<int>> ipc_send_order_;  // peer -> message ids in the peer's consumer order
   std::map<int, size_t> ipc_send_next_;             // peer -> next position in that order
   std::map<int, std::pair<BufPtr, cudaEvent_t>> ipc_ready_;  // produced, not yet issued
   void ipc_flush(DeviceState& d, int peer);
@@ -275,11 +278,23 @@ class Runtime {
   // rank = replica * P + pipeline device.  The arena's flag region also holds
   // ready[D] / done[D] for the gradient all-reduce of this pipeline device.
   int replicas_ = 1, replica_ = 0;
-  std::vector<float*> dp_grads_;     // replica -> that replica's grad buffer (mapped; own = local)
+  // Gradient group of this rank: the global ranks whose gradient buffers are
+  // reduced with its own at the OptimizerStep -- the same pipeline device in
+  // every replica, plus, for Chimera, the mirrored device P-1-p that holds the
+  // same two stages for the opposite direction.  Summed, then scaled by 1/D.
+  std::vector<int> grad_group_;      // sorted global ranks (includes this rank)
+  int group_me_ = 0;                 // this rank's index in grad_group_
+  float grad_scale_ = 1.f;
+  std::vector<float*> dp_grads_;     // group index -> that rank's grad buffer (mapped; own = local)
   float** dp_grads_dev_ = nullptr;   // same table in device memory (kernel argument)
   int grank(int replica, int pipe) const { return replica * list_.config.devices + pipe; }
-  uint32_t* ipc_dp_flag(char* base, int which, int replica) const {
-    return reinterpret_cast<uint32_t*>(base) + 2 * ipc_msgs_.size() + which * replicas_ + replica;
+  // Chimera places stage p (down) and P-1-p (up) on device p: devices p and
+  // P-1-p hold the same two stages and sum their gradients.
+  int chimera_mirror() const {
+    return list_.config.scheme == wavepipe::Scheme::Chimera ? list_.config.devices - 1 - rank_ : rank_;
+  }
+  uint32_t* ipc_dp_flag(char* base, int which, int member) const {
+    return reinterpret_cast<uint32_t*>(base) + 2 * ipc_msgs_.size() + which * grad_group_.size() + member;
   }
   void dp_allreduce(DeviceState& d);
   void ipc_setup();

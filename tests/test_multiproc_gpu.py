@@ -57,7 +57,7 @@ def _run(rt, params, B, desc, steps, update, replica=0):
     return losses, grads
 
 
-def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q, D=1):
+def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q, D=1, scheme="Hanayo"):
     import faulthandler
     import sys
     import torch.distributed as dist
@@ -73,7 +73,7 @@ def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q, D=1):
         torch.cuda.set_device(dev)
         desc = _desc(dtype, optimizer)
         P = world // D
-        sched = wp.generate_schedule(wp.make_config(wp.Scheme.Hanayo, P, B, W, D))
+        sched = wp.generate_schedule(wp.make_config(getattr(wp.Scheme, scheme), P, B, W, D))
         rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_IPC, device_ids=[dev], rank=rank)
         ok, why = rt.ipc_status()
         assert ok, why  # the set-up probe of every mapped peer (copy + stream-op write)
@@ -124,12 +124,12 @@ def _spawn(world, B, W, dtype, optimizer="sgd", steps=1, update=False, D=1):
     return losses, grads
 
 
-def _spawn_raw(world, B, W, dtype, optimizer="sgd", steps=1, update=False, D=1):
+def _spawn_raw(world, B, W, dtype, optimizer="sgd", steps=1, update=False, D=1, scheme="Hanayo"):
     """Per-rank (losses, grads) of a spawned job."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, B, W, dtype, optimizer, steps, update, q, D))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, B, W, dtype, optimizer, steps, update, q, D, scheme))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -219,3 +219,36 @@ def test_data_parallel_replicas_equal_sequential_big_batch(P, D, B, W):
 def test_data_parallel_bf16_adamw_steps():
     losses = _spawn_raw(2, 4, 2, "bf16", optimizer="adamw", steps=3, update=True, D=2)[0][0]
     assert losses[2] < losses[0]
+
+
+@pytest.mark.parametrize("P,D,B", [(2, 1, 4), (4, 1, 8), (2, 2, 4)])
+def test_chimera_mirrored_stages_equal_oracle(P, D, B):
+    """Chimera (the reference's bidirectional baseline, src/placement.cpp:41-50):
+    device p holds stage p for the down pipeline and stage P-1-p for the up
+    one, so devices p and P-1-p hold the same stages and their gradients are
+    summed over peer memory at the optimizer step (with the D replicas, then
+    scaled by 1/D).  fp32 loss and every gradient equal the fp64 oracle's
+    sequential step over the D*B microbatches, bit-identical on all holders."""
+    from oracle import model as om
+    from paper_2308_15762_b200.data import synthetic_batch
+    out = _spawn_raw(P * D, B, 1, "fp32", D=D, scheme="Chimera")
+    desc = _desc("fp32")
+    params = om.init_params(desc, seed=21)
+    tokens, labels = synthetic_batch(B * D, desc.micro_batch_size, desc.seq, desc.vocab)
+    want_loss, want = om.reference_step(params, tokens, labels, desc)
+    assert abs(out[0][0][0] - want_loss) <= 1e-5 * abs(want_loss)
+    for rank, (_, grads) in out.items():
+        for n, g in grads.items():
+            w = want[n].numpy().ravel().astype(np.float64)
+            e = np.linalg.norm(g - w) / max(np.linalg.norm(w), 1e-30)
+            assert e <= 1e-5, (rank, n, e)
+        mirror = (rank // P) * P + P - 1 - rank % P
+        for n, g in grads.items():
+            assert np.array_equal(g, out[mirror][1][n]), (rank, n)
+
+
+def test_chimera_needs_ipc_transport():
+    import paper_2308_15762_b200 as wp
+    sched = wp.generate_schedule(wp.make_config(wp.Scheme.Chimera, 2, 4))
+    with pytest.raises(Exception, match="IPC transport"):
+        wp.Runtime(_desc("fp32"), sched, device_ids=[0, 0])
