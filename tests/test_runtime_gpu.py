@@ -76,6 +76,15 @@ def test_fp32_baseline_schemes_untied(scheme, P, B):
     run_parity(desc, P, B, 1, scheme=scheme)
 
 
+@pytest.mark.parametrize("P,B,W", [(2, 4, 2), (4, 8, 1)])
+def test_fp32_chimera_wave(P, B, W):
+    """Chimera-wave (ref src/placement.cpp:79-80: Hanayo placement) runs on
+    the in-process runtime like Hanayo: the V-shaped slices keep the
+    embedding and the tied head on device 0."""
+    desc = wp.ModelDesc(**dict(TINY, layers=2), dtype="fp32")
+    run_parity(desc, P, B, W, scheme=wp.Scheme.ChimeraWave)
+
+
 def test_fp32_sgd_and_adamw_update():
     for opt in ("sgd", "adamw"):
         desc = wp.ModelDesc(**dict(TINY, layers=1), dtype="fp32", optimizer=opt, lr=1e-2, weight_decay=0.01)
