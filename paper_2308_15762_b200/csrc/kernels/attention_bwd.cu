@@ -8,8 +8,13 @@
 //              dS^T = P^T * (dP^T - Delta) / sqrt(D)  -> bf16 -> smem (SW128)
 //   MMA        dV_j += P^T dO_i,  dK_j += dS^T Q_i        (TMEM accumulators)
 //              dQ_i  = dS K_j     (A = the dS^T tile read MN-major)
-//   dQ warps   4 warps drain dQ_i from TMEM with red.global.add.v4.f32 into an
-//              fp32 accumulator (every key tile contributes to each q tile)
+//   dQ warps   4 warps drain dQ_i from TMEM through their own fp32 SW128
+//              slabs with TMA bulk reduce-adds into an fp32 accumulator
+//              (every key tile contributes to each q tile)
+// Issue order per q tile: dV_j(i), S^T(i+1) (into the P^T columns dV just
+// read), dK_j(i), dQ_i, then dP^T(i+1) once dQ_i is out of TMEM -- so the
+// softmax of tile i+1 overlaps dK/dQ of tile i and the dQ drain, whose L2
+// reduce-adds no longer hold the dS^T buffer.
 // Delta = rowsum(dO * O) comes from attn_bwd_prep; dq_finish converts the fp32
 // dQ accumulator to bf16 into dqkv.  dK, dV are written at the end.
 #include <cuda.h>
@@ -36,8 +41,9 @@ template <int D>
 struct BwCfg {
   static constexpr int TILE = T128 * D * 2;     // K, V, Q, dO tiles
   static constexpr int PT = T128 * T128 * 2;    // dS^T tile
-  // K, V, Q[2], dO[2], dS^T, lse/delta (single-buffered), barriers
-  static constexpr int SMEM = 6 * TILE + PT + 2 * T128 * 4 + 1024 + 256;
+  static constexpr int STAGE = 4 * 2 * SLAB_BYTES;  // dQ drain: 2 fp32 slabs per drain warp
+  // K, V, Q[2], dO, dS^T, drain slabs, lse/delta (single-buffered), barriers
+  static constexpr int SMEM = 5 * TILE + PT + STAGE + 2 * T128 * 4 + 1024 + 256;
   static constexpr uint32_t kColDK = kColDV + D;
 };
 
@@ -97,14 +103,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   uint8_t* sK = smem;
   uint8_t* sV = sK + Cfg::TILE;
   uint8_t* sQ = sV + Cfg::TILE;       // [2]
-  uint8_t* sDO = sQ + 2 * Cfg::TILE;  // [2]
-  uint8_t* sDS = sDO + 2 * Cfg::TILE; // dS^T [keys x queries]
-  float* sLse = reinterpret_cast<float*>(sDS + Cfg::PT);  // [128]
+  uint8_t* sDO = sQ + 2 * Cfg::TILE;  // single
+  uint8_t* sDS = sDO + Cfg::TILE;     // dS^T [keys x queries]
+  uint8_t* sStage = sDS + Cfg::PT;    // dQ drain slabs
+  float* sLse = reinterpret_cast<float*>(sStage + Cfg::STAGE);  // [128]
   float* sDelta = sLse + T128;                            // [128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sDelta + T128);
   uint64_t* kv_full = bars + 0;
-  uint64_t* qdo_full = bars + 1;   // [2]
-  uint64_t* qdo_empty = bars + 3;  // [2]
+  uint64_t* q_full = bars + 1;   // [2]
+  uint64_t* q_empty = bars + 3;  // [2]
   uint64_t* s_full = bars + 5;
   uint64_t* ds_full = bars + 6;
   uint64_t* pds_free = bars + 7;
@@ -112,7 +119,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   uint64_t* dq_free = bars + 9;
   uint64_t* dkv_done = bars + 10;
   uint64_t* dp_full = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* do_full = bars + 12;
+  uint64_t* do_empty = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // Heaviest-first (LPT) order: all (batch, head) CTAs of key tile 0 -- the
@@ -131,12 +140,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   if (warp == 1 && lane == 0) {
     mbar_init(kv_full, 1);
     for (int x = 0; x < 2; ++x) {
-      mbar_init(&qdo_full[x], 1);
-      mbar_init(&qdo_empty[x], 1);
+      mbar_init(&q_full[x], 1);
+      mbar_init(&q_empty[x], 1);
     }
+    mbar_init(do_full, 1);
+    mbar_init(do_empty, 1);
     mbar_init(s_full, 1);
     mbar_init(ds_full, 8);
-    mbar_init(pds_free, 5);  // dQ MMA commit + the 4 drain warps' slab reads
+    mbar_init(pds_free, 1);  // dK and dQ MMAs done reading dS^T
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 4);
     mbar_init(dkv_done, 1);
@@ -161,15 +172,18 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         tma_load_4d(&map_k, kv_full, sK + a * ATOM, a * 64, head, kj * T128, b);
         tma_load_4d(&map_v, kv_full, sV + a * ATOM, a * 64, head, kj * T128, b);
       }
-      for (int it = 0; it < n_it; ++it) {  // Q / dO double-buffered: up to two tiles ahead
+      for (int it = 0; it < n_it; ++it) {  // Q double-buffered (two tiles ahead), dO single
         const int qi = i0 + it, x = it & 1;
-        if (it >= 2) mbar_wait(&qdo_empty[x], ((it - 2) >> 1) & 1);
-        mbar_expect_tx(&qdo_full[x], 2 * Cfg::TILE);
+        if (it >= 2) mbar_wait(&q_empty[x], ((it - 2) >> 1) & 1);
+        mbar_expect_tx(&q_full[x], Cfg::TILE);
 #pragma unroll
-        for (int a = 0; a < D / 64; ++a) {
-          tma_load_4d(&map_q, &qdo_full[x], sQ + x * Cfg::TILE + a * ATOM, a * 64, head, qi * T128, b);
-          tma_load_4d(&map_do, &qdo_full[x], sDO + x * Cfg::TILE + a * ATOM, a * 64, head, qi * T128, b);
-        }
+        for (int a = 0; a < D / 64; ++a)
+          tma_load_4d(&map_q, &q_full[x], sQ + x * Cfg::TILE + a * ATOM, a * 64, head, qi * T128, b);
+        if (it >= 1) mbar_wait(do_empty, (it - 1) & 1);  // dV(it-1) read dO(it-1)
+        mbar_expect_tx(do_full, Cfg::TILE);
+#pragma unroll
+        for (int a = 0; a < D / 64; ++a)
+          tma_load_4d(&map_do, do_full, sDO + a * ATOM, a * 64, head, qi * T128, b);
       }
     }
   } else if (warp == 1) {
@@ -192,7 +206,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       auto issue_s = [&](int it) {
         const int x = it & 1;
         const uint64_t dQ = make_desc(smem_u32(sQ + x * Cfg::TILE), 16, 1024);
-        mbar_wait(&qdo_full[x], (it >> 1) & 1);
+        mbar_wait(&q_full[x], (it >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
@@ -201,12 +215,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         }
         tc_commit(s_full);
       };
+      const uint64_t dDO = make_desc(smem_u32(sDO), 16, 1024), dDOm = make_desc(smem_u32(sDO), ATOM, 1024);
       auto issue_dp = [&](int it) {
-        const uint64_t dDO = make_desc(smem_u32(sDO + (it & 1) * Cfg::TILE), 16, 1024);
-        if (it > 0) {
-          mbar_wait(dq_free, (it - 1) & 1);  // dQ(it-1) drained from the dP^T columns
-          tc_fence_after();
-        }
+        if (it > 0) mbar_wait(dq_free, (it - 1) & 1);  // dQ(it-1) out of the dP^T columns
+        mbar_wait(do_full, it & 1);
+        tc_fence_after();
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * ATOM + (k & 3) * 32;
@@ -218,20 +231,24 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       issue_dp(0);
       for (int it = 0; it < n_it; ++it) {
         const int x = it & 1;
-        const uint32_t aQ = smem_u32(sQ + x * Cfg::TILE), aDO = smem_u32(sDO + x * Cfg::TILE);
-        const uint64_t dDOm = make_desc(aDO, ATOM, 1024), dQm = make_desc(aQ, ATOM, 1024);
+        const uint64_t dQm = make_desc(smem_u32(sQ + x * Cfg::TILE), ATOM, 1024);
         mbar_wait(ds_full, it & 1);
         tc_fence_after();
-        // dV += P^T dO (P^T from TMEM: queries [0,64) at columns 0.., [64,128) at 64..),
+        // dV += P^T dO (P^T from TMEM: queries [0,64) at columns 0.., [64,128) at 64..)
+#pragma unroll
+        for (int k = 0; k < T128 / 16; ++k)
+          tc_mma_ts(tmem + kColDV, tmem + kColS + (k >> 2) * 64 + (k & 3) * 8, desc_add(dDOm, k * 2048), id_kv,
+                    (it | k) != 0);
+        tc_commit(do_empty);
+        // S^T(it+1) over the P^T(it) columns: in order after dV(it), which read them
+        if (it + 1 < n_it) issue_s(it + 1);
         // dK += dS^T Q (reduction over the 128 queries)
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k) {
           const uint32_t offa = (k >> 2) * ATOM + (k & 3) * 32;
-          tc_mma_ts(tmem + kColDV, tmem + kColS + (k >> 2) * 64 + (k & 3) * 8, desc_add(dDOm, k * 2048), id_kv,
-                    (it | k) != 0);
           tc_mma(tmem + Cfg::kColDK, desc_add(dDS, offa), desc_add(dQm, k * 2048), id_kv, (it | k) != 0);
         }
-        tc_commit(&qdo_empty[x]);
+        tc_commit(&q_empty[x]);
         // dQ = dS K (reduction over the 128 keys; dS^T tile read M-major)
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k) {
@@ -239,10 +256,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         }
         tc_commit(dq_full);
         tc_commit(pds_free);
-        if (it + 1 < n_it) {
-          issue_s(it + 1);   // overwrites the P^T(it) columns: in order after dV(it), which read them
-          issue_dp(it + 1);  // after the drain of dQ(it)
-        }
+        if (it + 1 < n_it) issue_dp(it + 1);  // after the drain read dQ(it) out of TMEM
       }
       tc_commit(dkv_done);
     }
@@ -286,18 +300,26 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           pk[i] = *reinterpret_cast<uint32_t*>(&hh);
         }
         tmem_st16(tmem + lb + kColS + half * 64 + h2 * 16, pk);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pv[h2 * 32 + i] *= p.scale;  // dS = (dP - Delta) * (P / sqrt(D))
       }
       // Phase B: dS^T = P^T * (dP^T - Delta) / sqrt(D) once dP^T is in.
       mbar_wait(dp_full, it & 1);
       tc_fence_after();
-      if (it > 0) mbar_wait(pds_free, (it - 1) & 1);  // dS^T buffer free (dK, dQ, drain done)
+      if (it > 0) mbar_wait(pds_free, (it - 1) & 1);  // dS^T buffer free (dK(it-1), dQ(it-1) read it)
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
         const int c0 = half * 64 + h2 * 32;
         float dp[32], ds[32];
         tmem_ld32(tmem + lb + kColDP + c0, dp);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) ds[i] = pv[h2 * 32 + i] * (dp[i] - dl[c0 + i]) * p.scale;
+        for (int i = 0; i < 32; i += 4) {
+          const float4 d4 = *reinterpret_cast<const float4*>(dl + c0 + i);
+          ds[i] = pv[h2 * 32 + i] * (dp[i] - d4.x);
+          ds[i + 1] = pv[h2 * 32 + i + 1] * (dp[i + 1] - d4.y);
+          ds[i + 2] = pv[h2 * 32 + i + 2] * (dp[i + 2] - d4.z);
+          ds[i + 3] = pv[h2 * 32 + i + 3] * (dp[i + 3] - d4.w);
+        }
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           uint4 ud;
@@ -338,40 +360,50 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     }
   } else if (warp >= 12) {
     // ------------------------------------------------ dQ drain (query rows)
-    // TMEM -> fp32 SW128 slabs (staged in the dS^T buffer, free once the dQ
-    // MMA that read it is done) -> TMA bulk reduce-add into dq_acc: whole
-    // 128-byte row segments reduced in L2 instead of per-lane atomics.
+    // TMEM -> fp32 SW128 slabs (two per warp, in their own buffer) -> TMA
+    // bulk reduce-add into dq_acc: whole 128-byte row segments reduced in L2
+    // instead of per-lane atomics.  The row is read out of TMEM in two halves
+    // and dq_free is raised as soon as the second half is in registers, so
+    // the next dP^T overlaps the reduce-adds.
     const int ew = warp & 3;
     const uint32_t lb = static_cast<uint32_t>(ew * 32) << 16;
-    uint8_t* slabs = sDS + ew * 2 * SLAB_BYTES;
+    uint8_t* slabs = sStage + ew * 2 * SLAB_BYTES;
+    constexpr int NCH = D / 32, HALF = NCH / 2;
     for (int it = 0; it < n_it; ++it) {
       const int qi = i0 + it;
       mbar_wait(dq_full, it & 1);
       tc_fence_after();
       const int row0 = b * p.seq + qi * T128 + ew * 32;
-#pragma unroll 1
-      for (int c = 0; c < D; c += 32) {
-        uint8_t* sb = slabs + ((c / 32) & 1) * SLAB_BYTES;
-        if (lane == 0) bulk_wait_read<1>();
-        __syncwarp();
-        float v[32];
-        tmem_ld32(tmem + lb + kColDP + c, v);
-        slab_put_f32(sb, lane, v);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_reduce_add_2d(&map_dq, sb, head * D + c, row0);
-          bulk_commit();
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        uint32_t u[HALF][32];
+#pragma unroll
+        for (int c = 0; c < HALF; ++c) tmem_ld32_issue(tmem + lb + kColDP + (r * HALF + c) * 32, u[c]);
+        tmem_wait_ld();
+        float v[HALF][32];
+#pragma unroll
+        for (int c = 0; c < HALF; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[c][i] = __uint_as_float(u[c][i]);
+        if (r == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dq_free);  // dQ TMEM columns read out
+        }
+#pragma unroll
+        for (int c = 0; c < HALF; ++c) {
+          uint8_t* sb = slabs + ((r * HALF + c) & 1) * SLAB_BYTES;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          slab_put_f32(sb, lane, v[c]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_reduce_add_2d(&map_dq, sb, head * D + (r * HALF + c) * 32, row0);
+            bulk_commit();
+          }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_free);  // dQ TMEM columns read out
-      if (lane == 0) {
-        bulk_wait_read<0>();
-        mbar_arrive(pds_free);  // dS^T buffer no longer read by the reduce stores
-      }
-      __syncwarp();
     }
     if (lane == 0) bulk_wait<0>();
   }
