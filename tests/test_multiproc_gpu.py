@@ -37,9 +37,9 @@ def _free_port():
     return port
 
 
-def _desc(dtype, optimizer="sgd"):
+def _desc(dtype, optimizer="sgd", tie=True):
     import paper_2308_15762_b200 as wp
-    return wp.ModelDesc(**TINY, dtype=dtype, optimizer=optimizer, lr=1e-3, weight_decay=0.01)
+    return wp.ModelDesc(**TINY, dtype=dtype, optimizer=optimizer, lr=1e-3, weight_decay=0.01, tie_embeddings=tie)
 
 
 def _run(rt, params, B, desc, steps, update, replica=0):
@@ -71,7 +71,7 @@ def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q, D=1, sc
         ngpu = torch.cuda.device_count()
         dev = rank % ngpu
         torch.cuda.set_device(dev)
-        desc = _desc(dtype, optimizer)
+        desc = _desc(dtype, optimizer, tie=scheme not in ("GPipe", "Dapple"))
         P = world // D
         sched = wp.generate_schedule(wp.make_config(getattr(wp.Scheme, scheme), P, B, W, D))
         rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_IPC, device_ids=[dev], rank=rank)
@@ -252,3 +252,22 @@ def test_chimera_needs_ipc_transport():
     sched = wp.generate_schedule(wp.make_config(wp.Scheme.Chimera, 2, 4))
     with pytest.raises(Exception, match="IPC transport"):
         wp.Runtime(_desc("fp32"), sched, device_ids=[0, 0])
+
+
+@pytest.mark.parametrize("scheme,P,B", [("Dapple", 4, 8), ("GPipe", 2, 4)])
+def test_classic_schemes_over_ipc_equal_oracle(scheme, P, B):
+    """The baseline schemes (classic placement, src/placement.cpp:32-38; the
+    head on the last device, so untied) through the same IPC transport."""
+    from oracle import model as om
+    from paper_2308_15762_b200.data import synthetic_batch
+    out = _spawn_raw(P, B, 1, "fp32", scheme=scheme)
+    desc = _desc("fp32", tie=False)
+    params = om.init_params(desc, seed=21)
+    tokens, labels = synthetic_batch(B, desc.micro_batch_size, desc.seq, desc.vocab)
+    want_loss, want = om.reference_step(params, tokens, labels, desc)
+    assert abs(out[0][0][0] - want_loss) <= 1e-5 * abs(want_loss)
+    for rank, (_, grads) in out.items():
+        for n, g in grads.items():
+            w = want[n].numpy().ravel().astype(np.float64)
+            e = np.linalg.norm(g - w) / max(np.linalg.norm(w), 1e-30)
+            assert e <= 1e-5, (rank, n, e)
