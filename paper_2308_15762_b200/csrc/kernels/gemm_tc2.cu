@@ -435,19 +435,20 @@ int gemm_tc2(const GemmProblem& g, cudaStream_t s) {
   }
   // Split-K for the fp32 gradient accumulation (the TMA reduce-add epilogue
   // makes partial tiles commutative): a 2-way split when it fills the last
-  // wave of SM pairs better (measured: deeper splits and ranges shorter than
-  // 32 K-blocks lose more to pipeline fill and fp32 reduce traffic).
+  // wave of SM pairs better; 3-4 ways only for long K ranges (>= 64 blocks)
+  // and a clearly better last wave (shorter ranges lose more to pipeline
+  // fill and fp32 reduce traffic than the wave gains).
   p.k_split = 1;
   p.kb_per = p.k_blocks;
   static const bool split_off = std::getenv("WP_GEMM_NO_SPLITK") != nullptr;
   if (te && !split_off && g.epi.mode == kEpiAccum) {
     const int pairs = num_sms() / 2;
     double best = 0.0;
-    for (int s = 1; s <= 2 && p.k_blocks / s >= 32; ++s) {
+    for (int s = 1; s <= 4 && p.k_blocks / s >= (s <= 2 ? 32 : 64); ++s) {
       const int per = (p.k_blocks + s - 1) / s, parts = (p.k_blocks + per - 1) / per;
       const int64_t units = int64_t(p.num_tiles) * parts;
       const double eff = double(units) / (double((units + pairs - 1) / pairs) * pairs);
-      if (eff > best + 0.02) {
+      if (eff > best + (s <= 2 ? 0.02 : 0.06)) {
         best = eff;
         p.k_split = parts;
         p.kb_per = per;

@@ -124,7 +124,8 @@ def test_tc_pair_tma_epilogue_ragged(a_mn, b_mn, mode, shape):
     torch.testing.assert_close(out, ref, rtol=tol, atol=tol * 8)
 
 
-@pytest.mark.parametrize("shape", [(2048, 2048, 8192), (768, 512, 4096), (1024, 640, 2112)])
+@pytest.mark.parametrize("shape", [(2048, 2048, 8192), (768, 512, 4096), (1024, 640, 2112), (6144, 2048, 16384),
+                                   (1536, 512, 16384)])
 def test_tc_pair_split_k_accumulation(shape):
     """Weight-gradient shapes whose tile count underfills the last wave of SM
     pairs run split-K: partial tiles reduce-add into the fp32 gradient."""
