@@ -98,12 +98,24 @@ extern "C" int wp_debug_flash_fwd(int mbs, int seq, int heads, int head_dim, int
   }
 }
 
+extern "C" int wp_debug_flash_bwd_bias(int mbs, int seq, int heads, int head_dim, int causal, const void* qkv,
+                                       const void* out, const void* dout, const float* lse2, float* delta,
+                                       float* dq_acc, void* dqkv, float* dbias);
+
 extern "C" int wp_debug_flash_bwd(int mbs, int seq, int heads, int head_dim, int causal, const void* qkv,
                                   const void* out, const void* dout, const float* lse2, float* delta, float* dq_acc,
                                   void* dqkv) {
+  return wp_debug_flash_bwd_bias(mbs, seq, heads, head_dim, causal, qkv, out, dout, lse2, delta, dq_acc, dqkv,
+                                 nullptr);
+}
+
+// Same, also accumulating the QKV bias gradient (column sums of dQKV) into dbias.
+extern "C" int wp_debug_flash_bwd_bias(int mbs, int seq, int heads, int head_dim, int causal, const void* qkv,
+                                       const void* out, const void* dout, const float* lse2, float* delta,
+                                       float* dq_acc, void* dqkv, float* dbias) {
   try {
     wpk::AttnShape s{mbs, seq, heads, head_dim, heads * head_dim, causal};
-    wpk::flash_attn_bwd(s, qkv, out, dout, lse2, delta, dq_acc, dqkv, nullptr);
+    wpk::flash_attn_bwd(s, qkv, out, dout, lse2, delta, dq_acc, dqkv, nullptr, dbias);
     cudaError_t e = cudaDeviceSynchronize();
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return wpc::fail(WP_ERR_CUDA, std::string("flash bwd: ") + cudaGetErrorString(e));

@@ -23,8 +23,10 @@ int flash_attn_fwd(const AttnShape& s, const void* qkv, void* ctx, float* lse2, 
 // Backward: dqkv[:, 0:h) = dQ, [h, 2h) = dK, [2h, 3h) = dV from qkv, the
 // forward output `out` (ctx), its gradient `dout`, and lse2.  Scratch:
 // delta [mbs, heads, seq] fp32, dq_acc [T, h] fp32.  Returns launches issued.
+// dbias (optional, [3h] fp32): += the column sums of dQKV -- the QKV bias
+// gradient -- from the fp32 dK / dV accumulators and dQ before rounding.
 int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const void* dout, const float* lse2,
-                   float* delta, float* dq_acc, void* dqkv, cudaStream_t stream);
+                   float* delta, float* dq_acc, void* dqkv, cudaStream_t stream, float* dbias = nullptr);
 
 inline bool flash_supported(const AttnShape& s) {
   return s.seq % 128 == 0 && (s.head_dim == 64 || s.head_dim == 128);

@@ -76,6 +76,7 @@ struct BwParams {
   const float* delta;
   float* dq_acc;                // [T, h] fp32
   __nv_bfloat16* dqkv;          // [T, 3h]
+  float* dbias;                 // [3h] fp32 QKV bias gradient (+=), or null
 };
 
 __device__ __forceinline__ float ex2f(float x) {
@@ -356,6 +357,22 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(v[g + 2 * i], v[g + 2 * i + 1]);
           *reinterpret_cast<uint4*>(dst + c + g) = u;
         }
+        if (p.dbias) {
+          // bias gradient: column sums of this warp's 32 key rows (a
+          // transposing butterfly leaves column c + lane in v[0]), one
+          // atomic per column per warp
+#pragma unroll
+          for (int sh = 16; sh >= 1; sh >>= 1) {
+            const bool up = (lane & sh) != 0;
+#pragma unroll
+            for (int i = 0; i < sh; ++i) {
+              const float send = up ? v[i] : v[i + sh];
+              const float keep = up ? v[i + sh] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+            }
+          }
+          atomicAdd(p.dbias + (part ? 2 : 1) * p.hidden + head * D + c + lane, v[0]);
+        }
       }
     }
   } else if (warp >= 12) {
@@ -442,15 +459,47 @@ __global__ void attn_bwd_prep_k(const __nv_bfloat16* dout, const __nv_bfloat16* 
   }
 }
 
-// dqkv[:, 0:h] = bf16(dq_acc)
-__global__ void dq_finish_k(const float* dq, __nv_bfloat16* dqkv, int T, int hidden) {
-  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
-  if (i >= static_cast<int64_t>(T) * hidden) return;
-  const int64_t t = i / hidden, c = i % hidden;
-  const float4 v = *reinterpret_cast<const float4*>(dq + i);
-  __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(dqkv + t * 3 * hidden + c);
-  d[0] = __floats2bfloat162_rn(v.x, v.y);
-  d[1] = __floats2bfloat162_rn(v.z, v.w);
+// dqkv[:, 0:h] = bf16(dq_acc); with dbias, also += its column sums (the Q
+// part of the QKV bias gradient).  Block = 64 columns x 256 rows: thread
+// (x, y) converts 8 columns of rows y, y+32, ... (8 independent loads in
+// flight), then the 32 row-partials of each column meet in shared memory
+// and one atomic per column per block remains.
+constexpr int DQ_COLS = 64, DQ_ROWS = 256;
+__global__ void __launch_bounds__(256) dq_finish_k(const float* dq, __nv_bfloat16* dqkv, float* dbias, int T,
+                                                   int hidden) {
+  __shared__ float part[32][DQ_COLS + 1];
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int c = blockIdx.x * DQ_COLS + tx * 8;
+  const int t0 = blockIdx.y * DQ_ROWS;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c < hidden) {
+#pragma unroll
+    for (int k = 0; k < DQ_ROWS / 32; ++k) {
+      const int t = t0 + ty + 32 * k;
+      if (t >= T) break;
+      const float4 a = *reinterpret_cast<const float4*>(dq + static_cast<int64_t>(t) * hidden + c);
+      const float4 b = *reinterpret_cast<const float4*>(dq + static_cast<int64_t>(t) * hidden + c + 4);
+      uint4 u;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+      h[0] = __floats2bfloat162_rn(a.x, a.y);
+      h[1] = __floats2bfloat162_rn(a.z, a.w);
+      h[2] = __floats2bfloat162_rn(b.x, b.y);
+      h[3] = __floats2bfloat162_rn(b.z, b.w);
+      *reinterpret_cast<uint4*>(dqkv + static_cast<int64_t>(t) * 3 * hidden + c) = u;
+      acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+      acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+    }
+  }
+  if (!dbias) return;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) part[ty][tx * 8 + k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < DQ_COLS && blockIdx.x * DQ_COLS + threadIdx.x < hidden) {
+    float sum = 0.f;
+#pragma unroll 8
+    for (int y = 0; y < 32; ++y) sum += part[y][threadIdx.x];
+    atomicAdd(dbias + blockIdx.x * DQ_COLS + threadIdx.x, sum);
+  }
 }
 
 CUtensorMap bw_map(const void* base, const AttnShape& s, int64_t ld_elems) {
@@ -470,7 +519,7 @@ CUtensorMap bw_map(const void* base, const AttnShape& s, int64_t ld_elems) {
 
 template <int D>
 void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const float* lse2, const float* delta,
-                float* dq_acc, void* dqkv, cudaStream_t stream) {
+                float* dq_acc, void* dqkv, float* dbias, cudaStream_t stream) {
   auto* k = flash_bwd_kernel<D>;
   static uint64_t attr_done = 0;
   int dev = 0;
@@ -496,6 +545,7 @@ void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const flo
   p.delta = delta;
   p.dq_acc = dq_acc;
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
+  p.dbias = dbias;
   const int grid = p.n_tiles * s.heads * s.mbs;
   const CUtensorMap mdq = make_slab_map(dq_acc, kF32, s.hidden, int64_t(s.mbs) * s.seq, s.hidden);
   k<<<grid, BW_THREADS, BwCfg<D>::SMEM, stream>>>(mq, mk, mv, mdo, mdq, p);
@@ -506,7 +556,7 @@ void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const flo
 }  // namespace
 
 int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const void* dout, const float* lse2,
-                   float* delta, float* dq_acc, void* dqkv, cudaStream_t stream) {
+                   float* delta, float* dq_acc, void* dqkv, cudaStream_t stream, float* dbias) {
   if (s.seq % 128 || (s.head_dim != 64 && s.head_dim != 128)) {
     throw std::runtime_error("flash_attn_bwd: needs seq % 128 == 0 and head_dim in {64, 128}");
   }
@@ -516,11 +566,10 @@ int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const v
                                                        static_cast<const __nv_bfloat16*>(out), delta, T, s.heads,
                                                        s.head_dim, s.seq, s.hidden);
   cudaMemsetAsync(dq_acc, 0, sizeof(float) * T * s.hidden, stream);
-  if (s.head_dim == 128) launch_bwd<128>(s, qkv, dout, lse2, delta, dq_acc, dqkv, stream);
-  else launch_bwd<64>(s, qkv, dout, lse2, delta, dq_acc, dqkv, stream);
-  const int64_t n4 = static_cast<int64_t>(T) * s.hidden / 4;
-  dq_finish_k<<<static_cast<int>((n4 + 255) / 256), 256, 0, stream>>>(dq_acc, static_cast<__nv_bfloat16*>(dqkv), T,
-                                                                      s.hidden);
+  if (s.head_dim == 128) launch_bwd<128>(s, qkv, dout, lse2, delta, dq_acc, dqkv, dbias, stream);
+  else launch_bwd<64>(s, qkv, dout, lse2, delta, dq_acc, dqkv, dbias, stream);
+  const dim3 fin((s.hidden + DQ_COLS - 1) / DQ_COLS, (T + DQ_ROWS - 1) / DQ_ROWS);
+  dq_finish_k<<<fin, 256, 0, stream>>>(dq_acc, static_cast<__nv_bfloat16*>(dqkv), dbias, T, s.hidden);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("flash_attn_bwd: ") + cudaGetErrorString(e));
   return 3;

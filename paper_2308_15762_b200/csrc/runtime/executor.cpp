@@ -884,7 +884,7 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     dqkv = act(int64_t(T) * 3 * h);
     timed_attention(d, true, [&] {
       launches_ += wpk::flash_attn_bwd(attn_shape(), st.a->p, st.c->p, dctx->p, static_cast<float*>(st.b->p),
-                                       d.attn_delta, d.dq_acc, dqkv->p, cs);
+                                       d.attn_delta, d.dq_acc, dqkv->p, cs, grad(d, L + "attn.qkv.b"));
     });
   } else {
     // dP = dctx V^T  (fp32 scratch)
@@ -940,7 +940,8 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     }
   }
   wgrad(dqkv->p, 3 * h, st.ln->p, h, grad(d, L + "attn.qkv.w"));
-  launches_ += wpk::colsum_accum(dt, dqkv->p, grad(d, L + "attn.qkv.b"), T, 3 * h, 3 * h, cs);
+  if (!use_flash())  // the fused attention backward sums the QKV bias gradient itself
+    launches_ += wpk::colsum_accum(dt, dqkv->p, grad(d, L + "attn.qkv.b"), T, 3 * h, 3 * h, cs);
   BufPtr dln = act(int64_t(T) * h);
   dgrad(dqkv->p, 3 * h, 3 * h, weight(d, L + "attn.qkv.w"), h, dln->p, wpk::kEpiStore, nullptr, nullptr, L + "ln1");
   BufPtr dx = ln_bwd(dln, L + "ln1", dy);

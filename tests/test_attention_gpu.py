@@ -72,3 +72,35 @@ def test_flash_bwd(mbs, seq, heads, d, causal):
         want = ref[:, part * h:(part + 1) * h]
         err = (got - want).norm() / want.norm()
         assert err < 2e-2, (part, err.item())
+
+
+lib.wp_debug_flash_bwd_bias.restype = C.c_int
+lib.wp_debug_flash_bwd_bias.argtypes = [C.c_int] * 5 + [C.c_void_p] * 8
+
+
+@pytest.mark.parametrize("mbs,seq,heads,d,causal", [(2, 256, 2, 128, 1), (2, 384, 2, 64, 0)])
+def test_flash_bwd_fused_bias_grad(mbs, seq, heads, d, causal):
+    """The QKV bias gradient the backward accumulates (column sums of dQKV,
+    from the fp32 dK / dV accumulators and dQ) matches torch's dQKV.sum(0);
+    it adds to what the buffer held."""
+    torch.manual_seed(2)
+    h = heads * d
+    qkv = torch.randn(mbs * seq, 3 * h, device="cuda").bfloat16()
+    ctx = torch.empty(mbs * seq, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(mbs, heads, seq, device="cuda")
+    assert lib.wp_debug_flash_fwd(mbs, seq, heads, d, causal, qkv.data_ptr(), ctx.data_ptr(), lse.data_ptr()) == 0
+    dout = torch.randn(mbs * seq, h, device="cuda").bfloat16()
+    delta = torch.empty(mbs, heads, seq, device="cuda")
+    dq_acc = torch.empty(mbs * seq, h, device="cuda")
+    dqkv = torch.zeros(mbs * seq, 3 * h, device="cuda", dtype=torch.bfloat16)
+    dbias = torch.full((3 * h,), 0.5, device="cuda")
+    assert lib.wp_debug_flash_bwd_bias(mbs, seq, heads, d, causal, qkv.data_ptr(), ctx.data_ptr(), dout.data_ptr(),
+                                       lse.data_ptr(), delta.data_ptr(), dq_acc.data_ptr(), dqkv.data_ptr(),
+                                       dbias.data_ptr()) == 0, lib.wp_last_error()
+    x = qkv.float().requires_grad_(True)
+    o, _ = reference(x, mbs, seq, heads, d, causal)
+    o.backward(dout.float())
+    want = x.grad.sum(0) + 0.5
+    err = (dbias - want).norm() / (want - 0.5).norm()
+    assert err < 2e-2, err.item()
+
