@@ -360,6 +360,59 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_rows_k(const T* dy, const T* x,
   }
 }
 
+// Same dx, blocked 64 columns x 256 rows per CTA so the column sums of dx
+// (the bias gradient of the unit below: attention projection or FC2) come
+// out of the same pass: 32 row-partials per column meet in shared memory,
+// one atomic per column per block.
+template <typename T>
+__device__ __forceinline__ float round_to_t(float v) {
+  if constexpr (sizeof(T) == 2) return __bfloat162float(__float2bfloat16_rn(v));
+  else return v;
+}
+template <typename T>
+__global__ void __launch_bounds__(256) ln_bwd_dx_rows_cs_k(const T* dy, const T* x, const float* mean,
+                                                           const float* rstd, const float* w, const float* rows,
+                                                           const T* dres, T* dx, float* dcol, int T_, int h) {
+  __shared__ float part[32][65];
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int col = blockIdx.x * 64 + tx * 8;
+  const int t0 = blockIdx.y * 256;
+  const float inv_h = 1.f / h;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (col < h) {
+    float wv[8];
+    load8(w + col, wv);
+#pragma unroll 4
+    for (int k = 0; k < 8; ++k) {
+      const int row = t0 + ty + 32 * k;
+      if (row >= T_) break;
+      const int64_t off = static_cast<int64_t>(row) * h + col;
+      float d[8], xv[8], r[8], o[8];
+      load8(dy + off, d);
+      load8(x + off, xv);
+      if (dres) load8(dres + off, r);
+      const float mu = mean[row], rs = rstd[row], sg = rows[2 * row] * inv_h, sgx = rows[2 * row + 1] * inv_h;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = (xv[j] - mu) * rs;
+        o[j] = rs * (d[j] * wv[j] - sg - xh * sgx) + (dres ? r[j] : 0.f);
+      }
+      store8(dx + off, o);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += round_to_t<T>(o[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) part[ty][tx * 8 + j] = acc[j];
+  __syncthreads();
+  if (threadIdx.x < 64 && blockIdx.x * 64 + static_cast<int>(threadIdx.x) < h) {
+    float sum = 0.f;
+#pragma unroll 8
+    for (int y = 0; y < 32; ++y) sum += part[y][threadIdx.x];
+    atomicAdd(dcol + blockIdx.x * 64 + threadIdx.x, sum);
+  }
+}
+
 // dw, db: lane <-> column (coalesced), 8 warps stride over a row range, block
 // partials reduced in shared memory, one atomic per column per block.
 template <typename T>
@@ -820,8 +873,21 @@ int layernorm_bwd(int dtype, const void* dy, const void* x, const float* mean, c
 
 int layernorm_bwd_dx_rows(int dtype, const void* dy, const void* x, const float* mean, const float* rstd,
                           const float* w, const float* rows, const void* dres, void* dx, int T_, int h,
-                          cudaStream_t s) {
+                          cudaStream_t s, float* dcol) {
   if (h % 8) throw std::runtime_error("layernorm_bwd_dx_rows: hidden must be a multiple of 8");
+  if (dcol) {
+    const dim3 grid((h + 63) / 64, (T_ + 255) / 256);
+    if (dtype == kBF16)
+      ln_bwd_dx_rows_cs_k<bf16><<<grid, 256, 0, s>>>(static_cast<const bf16*>(dy), static_cast<const bf16*>(x), mean,
+                                                     rstd, w, rows, static_cast<const bf16*>(dres),
+                                                     static_cast<bf16*>(dx), dcol, T_, h);
+    else
+      ln_bwd_dx_rows_cs_k<float><<<grid, 256, 0, s>>>(static_cast<const float*>(dy), static_cast<const float*>(x),
+                                                      mean, rstd, w, rows, static_cast<const float*>(dres),
+                                                      static_cast<float*>(dx), dcol, T_, h);
+    check_launch("layernorm_bwd_dx_rows");
+    return 1;
+  }
   const int64_t n8 = static_cast<int64_t>(T_) * h / 8;
   const int grid = static_cast<int>(std::min<int64_t>((n8 + 255) / 256, 8 * sm_count()));
   if (dtype == kBF16)

@@ -27,8 +27,11 @@ int layernorm_bwd(int dtype, const void* dy, const void* x, const float* mean, c
 // dx of a LayerNorm backward whose dw / db and row sums were produced by the
 // dgrad GEMM's epilogue (GemmProblem::epi.ln_*): rows[2t] = sum_n dy*w,
 // rows[2t+1] = sum_n dy*w*xhat; dx = rstd (dy w - rows0/h - xhat rows1/h) + dres.
+// dcol (optional, fp32 [h]): += the column sums of dx (the bf16-rounded
+// values the next unit reads) -- the bias gradient of the unit below.
 int layernorm_bwd_dx_rows(int dtype, const void* dy, const void* x, const float* mean, const float* rstd,
-                          const float* w, const float* rows, const void* dres, void* dx, int T, int h, cudaStream_t s);
+                          const float* w, const float* rows, const void* dres, void* dx, int T, int h, cudaStream_t s,
+                          float* dcol = nullptr);
 
 // Row softmax of fp32 scores S [rows, n] -> P (act dtype); causal masks
 // column j > (row % n) (query position) and reads/writes only up to the end

@@ -51,6 +51,8 @@ struct DeviceState {
   float* attn_delta = nullptr;  // fp32 [mbs, heads, seq] (fused attention backward)
   float* dq_acc = nullptr;      // fp32 [T, h]             (fused attention backward)
   float* ln_rows = nullptr;     // fp32 [T, 2]  LayerNorm-backward row sums (GEMM-fused path)
+  int bwd_unit_lo = 0;          // first unit of the slice being run backward
+  bool dy_bias_done = false;    // the incoming dy's column sums are already in this unit's bias grad
   std::vector<std::pair<int, int>> be_partner;  // per position: (device, position) of a BE's counterpart
 
   // per-step program state

@@ -785,6 +785,8 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     b.reset();
   };
   const std::string L = "h." + std::to_string(u.layer) + ".";
+  const bool dy_bias_done = d.dy_bias_done;  // set by the unit above (same slice) for this dy
+  d.dy_bias_done = false;
 
   if (u.kind == UnitKind::Embed) {
     launches_ += wpk::embed_bwd(dt, d.tokens + int64_t(mb) * T, dy->p, grad(d, "wte"), grad(d, "wpe"), T, S, h, cs);
@@ -826,12 +828,27 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     g.epi.mode = wpk::kEpiAccum, g.epi.c = dW, g.epi.c_dtype = wpk::kF32, g.epi.ldc = n_in;
     gemm(d, g);
   };
+  // The unit below this one in the same slice (run next, same device) takes
+  // dx as its dy: with the fused LayerNorm its bias gradient -- the column
+  // sums of that dy -- comes out of the dx pass (proj.b below an MLP's ln2,
+  // fc2.b below an attention block's ln1 or the final LayerNorm).
+  static const bool bias_unfused = std::getenv("WP_BIAS_UNFUSED") != nullptr;  // A/B switch
+  auto below_bias = [&]() -> float* {
+    if (!ln_fused || bias_unfused || ui - 1 < d.bwd_unit_lo) return nullptr;
+    const Unit& v = units_[ui - 1];
+    const std::string Lv = "h." + std::to_string(v.layer) + ".";
+    if (v.kind == UnitKind::Attn) return grad(d, Lv + "attn.proj.b");
+    if (v.kind == UnitKind::Mlp) return grad(d, Lv + "mlp.fc2.b");
+    return nullptr;
+  };
   auto ln_bwd = [&](const BufPtr& dln, const std::string& name, const BufPtr& dres) {
     BufPtr dx = act(int64_t(T) * h);
     if (ln_fused) {  // dw, db, row sums came with dLN from the dgrad GEMM
+      float* dcol = below_bias();
       launches_ += wpk::layernorm_bwd_dx_rows(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p),
                                               static_cast<float*>(st.rstd->p), master(d, name + ".w"), d.ln_rows,
-                                              dres ? dres->p : nullptr, dx->p, T, h, cs);
+                                              dres ? dres->p : nullptr, dx->p, T, h, cs, dcol);
+      d.dy_bias_done = dcol != nullptr;
       return dx;
     }
     LnBwdCheck chk;
@@ -863,7 +880,7 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     // dU = (dY W2) * gelu'(U); the fc1 bias gradient (column sums of dU) in the same epilogue
     dgrad(dy->p, h, h, weight(d, L + "mlp.fc2.w"), f, du->p, wpk::kEpiDGelu, st.a->p, grad(d, L + "mlp.fc1.b"));
     wgrad(dy->p, h, st.b->p, f, grad(d, L + "mlp.fc2.w"));
-    launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "mlp.fc2.b"), T, h, h, cs);
+    if (!dy_bias_done) launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "mlp.fc2.b"), T, h, h, cs);
     wgrad(du->p, f, st.ln->p, h, grad(d, L + "mlp.fc1.w"));
     BufPtr dln = act(int64_t(T) * h);
     dgrad(du->p, f, f, weight(d, L + "mlp.fc1.w"), h, dln->p, wpk::kEpiStore, nullptr, nullptr, L + "ln2");
@@ -878,7 +895,7 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   BufPtr dctx = act(int64_t(T) * h);
   dgrad(dy->p, h, h, weight(d, L + "attn.proj.w"), h, dctx->p);
   wgrad(dy->p, h, st.c->p, h, grad(d, L + "attn.proj.w"));
-  launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "attn.proj.b"), T, h, h, cs);
+  if (!dy_bias_done) launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "attn.proj.b"), T, h, h, cs);
   BufPtr dqkv;
   if (use_flash()) {
     dqkv = act(int64_t(T) * 3 * h);
@@ -1016,7 +1033,10 @@ void Runtime::backward(DeviceState& d, const Action& a) {
   if (it == d.stash.end()) throw wavepipe::SimulationError("runtime: backward before forward");
   SliceStash st = std::move(it->second);
   d.stash.erase(it);
+  d.bwd_unit_lo = bounds_[s];
+  d.dy_bias_done = false;
   for (int u = bounds_[s + 1] - 1; u >= bounds_[s]; --u) dy = unit_bwd(d, u, b, st.units[u - bounds_[s]], dy);
+  d.dy_bias_done = false;
   if (s > 0) deliver(d, MsgKey{kGrad, b, s - 1}, dy);
 }
 
