@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_rows_k(const T* dy, const T* x,
   }
 }
 
-// Same dx, blocked 64 columns x 256 rows per CTA so the column sums of dx
+// Same dx, blocked 64 columns x 128 rows per CTA so the column sums of dx
 // (the bias gradient of the unit below: attention projection or FC2) come
 // out of the same pass: 32 row-partials per column meet in shared memory,
 // one atomic per column per block.
@@ -376,14 +376,14 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_rows_cs_k(const T* dy, const T*
   __shared__ float part[32][65];
   const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
   const int col = blockIdx.x * 64 + tx * 8;
-  const int t0 = blockIdx.y * 256;
+  const int t0 = blockIdx.y * 128;
   const float inv_h = 1.f / h;
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (col < h) {
     float wv[8];
     load8(w + col, wv);
-#pragma unroll 4
-    for (int k = 0; k < 8; ++k) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
       const int row = t0 + ty + 32 * k;
       if (row >= T_) break;
       const int64_t off = static_cast<int64_t>(row) * h + col;
@@ -876,7 +876,7 @@ int layernorm_bwd_dx_rows(int dtype, const void* dy, const void* x, const float*
                           cudaStream_t s, float* dcol) {
   if (h % 8) throw std::runtime_error("layernorm_bwd_dx_rows: hidden must be a multiple of 8");
   if (dcol) {
-    const dim3 grid((h + 63) / 64, (T_ + 255) / 256);
+    const dim3 grid((h + 63) / 64, (T_ + 127) / 128);
     if (dtype == kBF16)
       ln_bwd_dx_rows_cs_k<bf16><<<grid, 256, 0, s>>>(static_cast<const bf16*>(dy), static_cast<const bf16*>(x), mean,
                                                      rstd, w, rows, static_cast<const bf16*>(dres),
