@@ -3,6 +3,8 @@
 // Vectorised 16-byte accesses where the row is contiguous, one warp per row
 // for row-wise reductions (warp shuffles, no shared memory), block-level
 // partial sums + one global atomic per column for parameter gradients.
+#include <cstdlib>
+#include <type_traits>
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -133,6 +135,70 @@ __global__ void __launch_bounds__(256) ln_fwd_k(const T* x, const float* w, cons
   if (lane == 0) {
     mean[row] = mu;
     rstd[row] = rs;
+  }
+}
+
+// bf16 forward, persistent warps over rows with the next row's loads in
+// flight while the current one is reduced and written (the row kernel above
+// is load-latency bound).  Same per-lane summation order as ln_fwd_k.
+__device__ __forceinline__ void unpack8(const uint4& u, float* v) {
+  const bf16* hv = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(hv[i]);
+}
+template <int C>
+__global__ void __launch_bounds__(256) ln_fwd_pipe_k(const bf16* x, const float* w, const float* b, bf16* y,
+                                                     float* mean, float* rstd, int T_, int h) {
+  const int lane = threadIdx.x % 32;
+  const int nw = gridDim.x * (blockDim.x / 32);
+  int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (row >= T_) return;
+  uint4 cur[C], nxt[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    cur[c] = *reinterpret_cast<const uint4*>(x + static_cast<int64_t>(row) * h + c * 256 + lane * 8);
+  for (; row < T_; row += nw) {
+    if (row + nw < T_) {
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        nxt[c] = *reinterpret_cast<const uint4*>(x + static_cast<int64_t>(row + nw) * h + c * 256 + lane * 8);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float v[8];
+      unpack8(cur[c], v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += v[k];
+    }
+    const float mu = warp_sum(s) / h;
+    float q = 0.f;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float v[8];
+      unpack8(cur[c], v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) q += (v[k] - mu) * (v[k] - mu);
+    }
+    const float rs = rsqrtf(warp_sum(q) / h + 1e-5f);
+    bf16* yr = y + static_cast<int64_t>(row) * h;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int col = c * 256 + lane * 8;
+      float v[8], wv[8], bv[8], o[8];
+      unpack8(cur[c], v);
+      load8(w + col, wv);
+      load8(b + col, bv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = (v[k] - mu) * rs * wv[k] + bv[k];
+      store8(yr + col, o);
+    }
+    if (lane == 0) {
+      mean[row] = mu;
+      rstd[row] = rs;
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) cur[c] = nxt[c];
   }
 }
 
@@ -727,10 +793,22 @@ int grid_for(int64_t n, int block, int cap = 148 * 16) {
   return static_cast<int>(std::min<int64_t>((n + block - 1) / block, cap));
 }
 
+int sm_count();
+
 template <typename T>
 int ln_fwd_dispatch(const T* x, const float* w, const float* b, T* y, float* mean, float* rstd, int T_, int h,
                     cudaStream_t s) {
   const dim3 grid((T_ + 7) / 8), block(256);
+  static const bool pipe_off = std::getenv("WP_LN_FWD_ROWS") != nullptr;  // A/B switch
+  if constexpr (std::is_same_v<T, bf16>) {
+    if (!pipe_off && (h == 1024 || h == 2048)) {
+      const int blocks = std::max(1, std::min((T_ + 7) / 8, 2 * sm_count()));  // 2 CTAs per SM fit (<= 128 regs)
+      if (h == 1024) ln_fwd_pipe_k<4><<<blocks, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h);
+      else ln_fwd_pipe_k<8><<<blocks, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h);
+      check_launch("layernorm_fwd");
+      return 1;
+    }
+  }
   switch (h / 256) {
     case 1: ln_fwd_k<T, 1><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
     case 2: ln_fwd_k<T, 2><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
