@@ -28,6 +28,19 @@
 #include "kernels/tc_common.cuh"
 
 namespace wpk {
+#ifdef WP_BW_TRACE
+// Debug timeline of CTA 0 (build with -DWP_BW_TRACE; tools/bw_trace_probe.py):
+// clock64 per (event, q tile).
+__device__ unsigned long long g_bwt[16 * 32];
+#define BWT(ev, j)                                                                    \
+  do {                                                                                \
+    if (blockIdx.x == 0 && (j) < 32) g_bwt[(ev) * 32 + (j)] = clock64();             \
+  } while (0)
+#else
+#define BWT(ev, j) \
+  do {             \
+  } while (0)
+#endif
 namespace {
 
 using namespace tc;
@@ -219,8 +232,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       const uint64_t dDO = make_desc(smem_u32(sDO), 16, 1024), dDOm = make_desc(smem_u32(sDO), ATOM, 1024);
       auto issue_dp = [&](int it) {
         if (it > 0) mbar_wait(dq_free, (it - 1) & 1);  // dQ(it-1) out of the dP^T columns
+        BWT(13, it);
         mbar_wait(do_full, it & 1);
         tc_fence_after();
+        BWT(4, it);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * ATOM + (k & 3) * 32;
@@ -235,6 +250,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const uint64_t dQm = make_desc(smem_u32(sQ + x * Cfg::TILE), ATOM, 1024);
         mbar_wait(ds_full, it & 1);
         tc_fence_after();
+        BWT(1, it);
         // dV += P^T dO (P^T from TMEM: queries [0,64) at columns 0.., [64,128) at 64..)
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k)
@@ -243,6 +259,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         tc_commit(do_empty);
         // S^T(it+1) over the P^T(it) columns: in order after dV(it), which read them
         if (it + 1 < n_it) issue_s(it + 1);
+        BWT(3, it);
         // dK += dS^T Q (reduction over the 128 queries)
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k) {
@@ -257,6 +274,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         }
         tc_commit(dq_full);
         tc_commit(pds_free);
+        BWT(2, it);
         if (it + 1 < n_it) issue_dp(it + 1);  // after the drain read dQ(it) out of TMEM
       }
       tc_commit(dkv_done);
@@ -279,6 +297,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       named_bar(1, 256);
       mbar_wait(s_full, it & 1);
       tc_fence_after();
+      if (warp == 4 && lane == 0) BWT(5, it);
       const bool diag = p.causal && qi == kj;
       // Phase A: P^T = 2^(s*scale - lse) from S^T alone; kept in registers
       // for dS and written back over this half's S^T columns (bf16x2) as the
@@ -304,10 +323,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) pv[h2 * 32 + i] *= p.scale;  // dS = (dP - Delta) * (P / sqrt(D))
       }
+      if (warp == 4 && lane == 0) BWT(6, it);
       // Phase B: dS^T = P^T * (dP^T - Delta) / sqrt(D) once dP^T is in.
       mbar_wait(dp_full, it & 1);
       tc_fence_after();
-      if (it > 0) mbar_wait(pds_free, (it - 1) & 1);  // dS^T buffer free (dK(it-1), dQ(it-1) read it)
+      if (warp == 4 && lane == 0) BWT(7, it);
+      if (it > 0) mbar_wait(pds_free, (it - 1) & 1);
+      if (warp == 4 && lane == 0) BWT(8, it);
+  // dS^T buffer free (dK(it-1), dQ(it-1) read it)
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
         const int c0 = half * 64 + h2 * 32;
@@ -335,6 +358,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
+      if (warp == 4 && lane == 0) BWT(9, it);
     }
     // dK, dV rows of this key tile -> dqkv.
     mbar_wait(dkv_done, 0);
@@ -390,6 +414,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       const int qi = i0 + it;
       mbar_wait(dq_full, it & 1);
       tc_fence_after();
+      if (warp == 12 && lane == 0) BWT(10, it);
       const int row0 = b * p.seq + qi * T128 + ew * 32;
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
@@ -406,6 +431,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(dq_free);  // dQ TMEM columns read out
+          if (warp == 12 && lane == 0) BWT(11, it);
         }
 #pragma unroll
         for (int c = 0; c < HALF; ++c) {
@@ -576,3 +602,10 @@ int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const v
 }
 
 }  // namespace wpk
+
+#ifdef WP_BW_TRACE
+extern "C" int wp_debug_bw_trace(unsigned long long* out, int n) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, wpk::g_bwt, sizeof(unsigned long long) * (n < 512 ? n : 512)) == cudaSuccess ? 0 : 1;
+}
+#endif
