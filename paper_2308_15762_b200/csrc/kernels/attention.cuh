@@ -25,8 +25,11 @@ int flash_attn_fwd(const AttnShape& s, const void* qkv, void* ctx, float* lse2, 
 // delta [mbs, heads, seq] fp32, dq_acc [T, h] fp32.  Returns launches issued.
 // dbias (optional, [3h] fp32): += the column sums of dQKV -- the QKV bias
 // gradient -- from the fp32 dK / dV accumulators and dQ before rounding.
+// delta_ready: Delta = rowsum(dO * O) [mbs, heads, seq] is already in `delta`
+// (fused into the GEMM that produced dO); otherwise it is computed here.
 int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const void* dout, const float* lse2,
-                   float* delta, float* dq_acc, void* dqkv, cudaStream_t stream, float* dbias = nullptr);
+                   float* delta, float* dq_acc, void* dqkv, cudaStream_t stream, float* dbias = nullptr,
+                   bool delta_ready = false);
 
 inline bool flash_supported(const AttnShape& s) {
   return s.seq % 128 == 0 && (s.head_dim == 64 || s.head_dim == 128);

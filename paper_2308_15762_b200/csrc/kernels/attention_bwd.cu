@@ -582,15 +582,16 @@ void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const flo
 }  // namespace
 
 int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const void* dout, const float* lse2,
-                   float* delta, float* dq_acc, void* dqkv, cudaStream_t stream, float* dbias) {
+                   float* delta, float* dq_acc, void* dqkv, cudaStream_t stream, float* dbias, bool delta_ready) {
   if (s.seq % 128 || (s.head_dim != 64 && s.head_dim != 128)) {
     throw std::runtime_error("flash_attn_bwd: needs seq % 128 == 0 and head_dim in {64, 128}");
   }
   const int T = s.mbs * s.seq;
   const int64_t lanes = static_cast<int64_t>(T) * s.heads * (s.head_dim / 8);
-  attn_bwd_prep_k<<<static_cast<int>((lanes + 255) / 256), 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(dout),
-                                                       static_cast<const __nv_bfloat16*>(out), delta, T, s.heads,
-                                                       s.head_dim, s.seq, s.hidden);
+  if (!delta_ready)
+    attn_bwd_prep_k<<<static_cast<int>((lanes + 255) / 256), 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(dout), static_cast<const __nv_bfloat16*>(out), delta, T, s.heads,
+        s.head_dim, s.seq, s.hidden);
   cudaMemsetAsync(dq_acc, 0, sizeof(float) * T * s.hidden, stream);
   if (s.head_dim == 128) launch_bwd<128>(s, qkv, dout, lse2, delta, dq_acc, dqkv, dbias, stream);
   else launch_bwd<64>(s, qkv, dout, lse2, delta, dq_acc, dqkv, dbias, stream);
@@ -598,7 +599,7 @@ int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const v
   dq_finish_k<<<fin, 256, 0, stream>>>(dq_acc, static_cast<__nv_bfloat16*>(dqkv), dbias, T, s.hidden);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("flash_attn_bwd: ") + cudaGetErrorString(e));
-  return 3;
+  return delta_ready ? 2 : 3;
 }
 
 }  // namespace wpk

@@ -62,6 +62,15 @@ struct Epilogue {
   const float* ln_w = nullptr;
   float* ln_dw = nullptr;
   float* ln_rows = nullptr;
+  // Optional (store mode, bf16 C, CTA-pair TMA epilogue): per-row dot
+  // products of C (rounded to bf16) with rd_x (same dtype / ld as C) over
+  // column groups of rd_group, added into
+  //   rd_out[((m / rd_seq) * (N / rd_group) + n / rd_group) * rd_seq + m % rd_seq]
+  // -- attention's Delta = rowsum(dO * O) per (sequence, head, query) out of
+  // the projection data-gradient GEMM that produces dO.
+  const void* rd_x = nullptr;
+  float* rd_out = nullptr;
+  int rd_group = 0, rd_seq = 0;
 };
 
 // Causal structure inside each batch element (an s x s attention block,

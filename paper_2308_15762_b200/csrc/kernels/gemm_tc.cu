@@ -303,6 +303,7 @@ int gemm_tc(const GemmProblem& g, cudaStream_t s) {  // declared in gemm.cuh
   static const bool pair_off = std::getenv("WP_GEMM_NO_PAIR") != nullptr;
   if (!pair_off && g.causal == kCausalNone && g.M >= 256 && g.N > 128 && g.nb1 * g.nb2 == 1) return gemm_tc2(g, s);
   if (g.epi.ln_x) throw std::runtime_error("gemm: LayerNorm-backward partials need the CTA-pair kernel");
+  if (g.epi.rd_x) throw std::runtime_error("gemm: fused row dot products need the CTA-pair kernel");
   if (g.epi.colsum) {  // unfused path: the column sums as a separate pass
     if (g.nb1 * g.nb2 != 1) throw std::runtime_error("gemm: colsum needs an unbatched problem");
     GemmProblem g2 = g;

@@ -58,11 +58,13 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
   const bool needs_in = mode == kEpiResidual || mode == kEpiDGelu;
   uint8_t* sb = slabs + buf * SLAB_BYTES;
   const bool ln = CPC == 64 && e.ln_x != nullptr;  // LayerNorm-backward partials (store mode, bf16 C)
+  const bool rd = CPC == 64 && e.rd_x != nullptr;  // row dot products with rd_x (store mode, bf16 C)
+  const bool aux2 = ln || rd;                      // a second input slab, loaded into xb
   const int xb = buf ^ 1;                          // the LN input slab (buf flips below)
   uint8_t* sx = slabs + xb * SLAB_BYTES;
   if (lane == 0) {
     // the slab(s) about to be written must have been read out by earlier stores
-    if (mode == kEpiGelu || ln) bulk_wait_read<0>();
+    if (mode == kEpiGelu || aux2) bulk_wait_read<0>();
     else bulk_wait_read<1>();
   }
   __syncwarp();
@@ -70,7 +72,7 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
     mbar_expect_tx(&sbar[buf], SLAB_BYTES);
     tma_load_2d(map_x, &sbar[buf], sb, gcol, row0);
   }
-  if (ln && lane == 0) {
+  if (aux2 && lane == 0) {
     mbar_expect_tx(&sbar[xb], SLAB_BYTES);
     tma_load_2d(map_x, &sbar[xb], sx, gcol, row0);
   }
@@ -179,6 +181,20 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
       }
       const int col = gcol + 32 * q + lane;
       if (col < p.N) atomicAdd(e.ln_dw + col, w[0]);
+    }
+  }
+  if (rd) {
+    mbar_wait(&sbar[xb], (sphase >> xb) & 1);
+    sphase ^= 1u << xb;
+    float xv[CPC];
+    slab_get_bf16(sx, lane, xv);
+    const int row = row0 + lane;
+    if (row < p.M && gcol < p.N) {
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < CPC; ++i) acc += round_to(kBF16, v[i]) * xv[i];
+      const int64_t ngrp = p.N / e.rd_group;
+      atomicAdd(e.rd_out + (row / e.rd_seq * ngrp + gcol / e.rd_group) * e.rd_seq + row % e.rd_seq, acc);
     }
   }
   if (e.colsum) {
@@ -414,7 +430,8 @@ void launch_pair(const GemmProblem& g, const Params& p, cudaStream_t s) {
     mc = make_slab_map(e.c, dt, g.N, g.M, e.ldc);
     const void* x = e.mode == kEpiResidual ? e.resid
                     : (e.mode == kEpiGelu || e.mode == kEpiDGelu) ? e.aux
-                                                                  : e.ln_x;
+                    : e.ln_x                                      ? e.ln_x
+                                                                  : e.rd_x;
     mx = x ? make_slab_map(x, dt, g.N, g.M, e.ldc) : mc;
   }
   const int pairs = std::min(p.num_tiles * std::max(1, p.k_split), num_sms() / 2);
@@ -432,6 +449,11 @@ int gemm_tc2(const GemmProblem& g, cudaStream_t s) {
   const bool te = p.vec_ok && !te_off;
   if (g.epi.ln_x && (!te || g.epi.mode != kEpiStore || g.epi.c_dtype != kBF16)) {
     throw std::runtime_error("gemm: LayerNorm-backward partials need the TMA epilogue, store mode and a bf16 C");
+  }
+  if (g.epi.rd_x && (!te || g.epi.mode != kEpiStore || g.epi.c_dtype != kBF16 || g.epi.ln_x || g.epi.rd_group % 64 ||
+                     g.N % g.epi.rd_group || g.epi.rd_seq <= 0)) {
+    throw std::runtime_error("gemm: fused row dot products need the TMA epilogue, store mode, a bf16 C, no LN "
+                             "partials and 64-column-aligned groups");
   }
   // Split-K for the fp32 gradient accumulation (the TMA reduce-add epilogue
   // makes partial tiles commutative): a 2-way split when it fills the last

@@ -801,8 +801,16 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   static const bool ln_unfused = std::getenv("WP_LN_UNFUSED") != nullptr;
   const bool ln_fused = !ln_unfused && dt == wpk::kBF16 && T >= 256 && h > 128 && h % 8 == 0 &&
                         std::getenv("WP_GEMM_NO_PAIR") == nullptr && std::getenv("WP_GEMM_NO_TMA_EPI") == nullptr;
+  // Attention's Delta = rowsum(dO * O) out of the projection data-gradient
+  // GEMM that produces dO (its epilogue dots each 64-column slab of dO with
+  // the stashed O); WP_DELTA_UNFUSED=1 keeps the standalone pass (A/B).
+  static const bool delta_unfused = std::getenv("WP_DELTA_UNFUSED") != nullptr;
+  const bool delta_fused = !delta_unfused && use_flash() && dt == wpk::kBF16 && T >= 256 && h > 128 && h % 64 == 0 &&
+                           dh % 64 == 0 && std::getenv("WP_GEMM_NO_PAIR") == nullptr &&
+                           std::getenv("WP_GEMM_NO_TMA_EPI") == nullptr;
   auto dgrad = [&](const void* dY, int ld_dy, int n_out, const void* W, int n_in, void* dX, int mode = wpk::kEpiStore,
-                   const void* aux = nullptr, float* colsum = nullptr, const std::string& ln_name = std::string()) {
+                   const void* aux = nullptr, float* colsum = nullptr, const std::string& ln_name = std::string(),
+                   bool delta = false) {
     wpk::GemmProblem g;
     g.in_dtype = dt;
     g.M = T, g.N = n_in, g.K = n_out;
@@ -815,6 +823,10 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
       g.epi.ln_x = st.x->p, g.epi.ln_mean = static_cast<float*>(st.mean->p);
       g.epi.ln_rstd = static_cast<float*>(st.rstd->p), g.epi.ln_w = master(d, ln_name + ".w");
       g.epi.ln_dw = grad(d, ln_name + ".w"), g.epi.colsum = grad(d, ln_name + ".b"), g.epi.ln_rows = d.ln_rows;
+    }
+    if (delta) {
+      ck(cudaMemsetAsync(d.attn_delta, 0, sizeof(float) * size_t(T) * H, cs), "delta reset");
+      g.epi.rd_x = st.c->p, g.epi.rd_out = d.attn_delta, g.epi.rd_group = dh, g.epi.rd_seq = S;
     }
     gemm(d, g);
   };
@@ -893,7 +905,8 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   }
   // Attention block.
   BufPtr dctx = act(int64_t(T) * h);
-  dgrad(dy->p, h, h, weight(d, L + "attn.proj.w"), h, dctx->p);
+  dgrad(dy->p, h, h, weight(d, L + "attn.proj.w"), h, dctx->p, wpk::kEpiStore, nullptr, nullptr, std::string(),
+        delta_fused);
   wgrad(dy->p, h, st.c->p, h, grad(d, L + "attn.proj.w"));
   if (!dy_bias_done) launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "attn.proj.b"), T, h, h, cs);
   BufPtr dqkv;
@@ -901,7 +914,8 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     dqkv = act(int64_t(T) * 3 * h);
     timed_attention(d, true, [&] {
       launches_ += wpk::flash_attn_bwd(attn_shape(), st.a->p, st.c->p, dctx->p, static_cast<float*>(st.b->p),
-                                       d.attn_delta, d.dq_acc, dqkv->p, cs, grad(d, L + "attn.qkv.b"));
+                                       d.attn_delta, d.dq_acc, dqkv->p, cs, grad(d, L + "attn.qkv.b"),
+                                       delta_fused);
     });
   } else {
     // dP = dctx V^T  (fp32 scratch)
