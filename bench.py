@@ -18,14 +18,20 @@ host memory every step and the loss read back.  The per-step working set
 (~35 GB of weights, optimizer state and activations) is far larger than the
 126 MB L2, so no explicit flush is needed between steps.
 
-Multi-GPU (torchrun, one rank per GPU): rank r = pipeline device r; the
-inter-stage transport is the CUDA-IPC one (copy-engine pushes over NVLink
-into IPC-mapped landing slots, stream-memory-op flags; WP_TRANSPORT=nccl
-selects NCCL send/recv instead); fixed global batch (strong scaling); time =
-max over ranks.  The measured bubble merges every rank's trace (each
-relative to its own step start, taken right after a barrier).
-WP_BENCH_SHARE_GPU=1 maps every rank to cuda:0 (functional testing of the
-multi-process path on a 1-GPU box; not a measurement).
+Multi-GPU: one rank per GPU.  `--gpus N` (N > 1) outside torchrun re-launches
+itself under `torch.distributed.run` with N ranks; under torchrun WORLD_SIZE
+must equal --gpus.  Rank r = pipeline device r; the inter-stage transport is
+the CUDA-IPC one (copy-engine pushes over NVLink into IPC-mapped landing
+slots, stream-memory-op flags; no fallback: a failed peer probe stops the
+run); fixed global batch (strong scaling); time = max over ranks.  The
+measured bubble merges every rank's trace (each relative to its own step
+start, taken right after a barrier).  WP_BENCH_SHARE_GPU=1 maps every rank to
+cuda:0 (functional testing of the multi-process path on a 1-GPU box; not a
+measurement).
+
+The reference arm (`--impl reference`) never imports this repo's package: its
+workload description, inputs (oracle/data.py) and CPU step (oracle/model.py)
+are test infrastructure, so only the oracle runs in that process.
 """
 import argparse
 import json
@@ -113,6 +119,28 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def flops_per_sample(m):
+    """3 x forward FLOPs: L*(2*(4h^2+2hf) + a*s*h) + 2hV per token."""
+    a = 2 if m["causal"] else 4
+    h, f, s = m["hidden"], m["ffn"], m["seq"]
+    return 3.0 * s * (m["layers"] * (2 * (4 * h * h + 2 * h * f) + a * s * h) + 2 * h * m["vocab"])
+
+
+class Workload:
+    """The benched model's shape without the product library (the reference
+    arm and the CPU baseline use only this and oracle/)."""
+
+    def __init__(self, args):
+        self.m = dict(MODELS[getattr(args, "model", "gpt-1.3b-like")])
+        for k, v in self.m.items():
+            setattr(self, k, v)
+        self.micro_batch_size = args.mbs
+        self.tie_embeddings = True
+
+    def flops_per_sample(self):
+        return flops_per_sample(self.m)
+
+
 def model_desc(args):
     import paper_2308_15762_b200 as wp
     m = MODELS[getattr(args, "model", "gpt-1.3b-like")]
@@ -127,7 +155,7 @@ def cpu_port_sample(desc, threads=None):
     full model by FLOPs (work conservation, proj/tests/test_simulate.cpp:67-79)."""
     import torch
     from oracle import model as om
-    from paper_2308_15762_b200.data import synthetic_batch
+    from oracle.data import synthetic_batch
     threads = threads or os.cpu_count()
     torch.set_num_threads(threads)
 
@@ -148,7 +176,8 @@ def cpu_port_sample(desc, threads=None):
     h, f, s = desc.hidden, desc.ffn, desc.seq
     reduced = 3.0 * s * ((2 * (4 * h * h + 2 * h * f) + a * s * h) + 2 * h * desc.vocab)
     rate = reduced / dt
-    return rate / desc.flops_per_sample(), dt, threads
+    return rate / flops_per_sample(dict(layers=desc.layers, hidden=h, ffn=f, seq=s, vocab=desc.vocab,
+                                        causal=desc.causal)), dt, threads
 
 
 def ref_schedule_time(P, B, W):
@@ -169,18 +198,19 @@ def run_reference(args, rank, world):
     this box's host cores (rank 0 only)."""
     if rank != 0:
         return
-    desc = model_desc(args)
+    desc = Workload(args)
+    P = args.gpus
     for _ in range(args.warmup):
         cpu_port_sample(desc)
     vals, per = [], []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, dt, cores = cpu_port_sample(desc)
+        v, dt, cores = cpu_port_sample(Workload(args))
         vals.append(v)
         per.append(dt)
     wall = time.perf_counter() - t0
     value = statistics.median(vals)
-    ref_ms = ref_schedule_time(args.gpus, args.microbatches, args.waves)
+    ref_ms = ref_schedule_time(P, args.microbatches, args.waves)
     sample = (f"1 sequence x (embedding + 1 of {desc.layers} layers + LM head) of {args.model}, fp32 torch CPU "
               f"fwd+bwd ({statistics.median(per):.2f} s), extrapolated to the full model by FLOPs; "
               f"schedule generate+simulate by the reference's own code (oracle/_ref): "
@@ -190,7 +220,7 @@ def run_reference(args, rank, world):
         "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic tokens (splitmix64), random-init weights",
-        "config": workload_config(args, world),
+        "config": workload_config(args, P * args.replicas),
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -223,6 +253,19 @@ def l2_note(m, P):
     return "working set (%.0f MB) fits in L2: functional preset, not a timing configuration" % (ws / 1e6)
 
 
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_command(n, argv):
+    """torchrun command line running this script on n ranks of this node."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + list(argv)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -240,7 +283,12 @@ def main():
     ap.add_argument("--gemm-report", action="store_true", help="per-shape GEMM table on stderr")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "wavepipe":
+        # One process per GPU: re-launch under torchrun with --gpus ranks.
+        os.execv(sys.executable, spawn_command(args.gpus, sys.argv[1:]))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "wavepipe" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch N ranks for --gpus N")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
@@ -261,7 +309,6 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    args.gpus = world
     D = args.replicas
     if world % D:
         raise SystemExit("--replicas must divide the number of ranks")
@@ -270,29 +317,14 @@ def main():
     desc = model_desc(args)
     cfg = wp.make_config(wp.Scheme.Hanayo, P, args.microbatches, args.waves, D)
     sched = wp.generate_schedule(cfg)
-    transport = os.environ.get("WP_TRANSPORT", "ipc")
-
-    def nccl_runtime():
-        obj = [wp.runtime.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        return wp.Runtime(desc, sched, transport=wp.TRANSPORT_NCCL, device_ids=[dev], rank=rank, nccl_id=obj[0])
-
-    if world > 1 and transport == "nccl" and D == 1:
-        rt = nccl_runtime()
-    elif world > 1:
+    transport = "ipc"
+    if world > 1:
         rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_IPC, device_ids=[dev], rank=rank)
         ok, why = rt.ipc_status()
         flag = torch.tensor([1 if ok else 0], device="cpu" if share else "cuda")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()) == 0:
-            # an unsupported peer path on this box: every rank switches together
-            if not ok:
-                print(f"rank {rank}: IPC transport probe failed ({why}); falling back to NCCL", file=sys.stderr)
-            if D > 1:
-                raise SystemExit("data-parallel replicas need the IPC transport")
-            rt.close()
-            transport = "nccl"
-            rt = nccl_runtime()
+            raise SystemExit(f"rank {rank}: CUDA-IPC peer probe failed on this box ({why or 'a peer failed'})")
     else:
         rt = wp.Runtime(desc, sched, device_ids=[dev])
 
@@ -349,6 +381,7 @@ def main():
     sec_prof, _ = timed(prof_steps, host=False)
     g_launches, g_flops, g_sec = rt.gemm_stats()
     a_launches, a_flops, a_sec = rt.attn_stats()
+    hbm_raw = rt.hbm_stats()
     if args.gemm_report and rank == 0:
         print(rt.gemm_report(), file=sys.stderr, flush=True)
     rt.set_profiling(False)
@@ -400,19 +433,38 @@ def main():
     peaks, peaks_kind = load_peaks()
     peak_tc = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
     achieved = g_flops / g_sec / 1e12 if g_sec > 0 else None
-    # DRAM bytes of one launch of the dominant GEMM (FC1 forward, the most
-    # expensive shape) from an ncu --set full capture (tools/gemm_traffic.py),
-    # next to its algorithmic bytes.
-    traffic, traffic_info = None, None
+    # DRAM bytes per launch (ncu --set full, tools/traffic.py) of the dominant
+    # GEMM (FC1 forward, the most expensive shape) and of the attention
+    # backward, next to their algorithmic bytes -- used only when captured at
+    # this run's shapes.
+    traffic_all = {}
     try:
-        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
-            tj = json.load(f)
-        traffic = tj.get("bytes_per_launch")
-        traffic_info = {"shape_mnk": tj.get("shape"), "algorithmic_bytes": tj.get("algorithmic_bytes"),
-                        "ratio": tj.get("ratio")}
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic_all = json.load(f)
     except (OSError, ValueError):
         pass
-    flops_step = desc.flops_per_sample() * args.microbatches * args.mbs * D
+    T = args.mbs * desc.seq
+
+    def traffic_for(key, shape):
+        t = traffic_all.get(key)
+        if not t or list(t.get("shape", [])) != list(shape):
+            return None
+        return {k: t.get(k) for k in ("shape", "bytes_per_launch", "algorithmic_bytes", "ratio", "source")}
+
+    fc1 = traffic_for("gemm_fc1", [T, desc.ffn, desc.hidden])
+    attn_bwd_traffic = traffic_for("flash_bwd", [args.mbs, desc.heads, desc.seq, desc.hidden // desc.heads,
+                                                 int(desc.causal)])
+    hbm_peak = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
+    hbm = {"peak_gbs": hbm_peak, "peak_kind": f"{peaks_kind} STREAM-style copy", "kernels": {},
+           "share_of_step": sum(v[2] for v in hbm_raw.values()) / sec_prof if sec_prof > 0 else None,
+           "bytes": "algorithmic (reads + writes of the tensors each launch must touch), per launch"}
+    for name, (n, b, t) in sorted(hbm_raw.items()):
+        if n == 0 or t <= 0:
+            continue
+        hbm["kernels"][name] = {"launches_per_step": n / prof_steps, "bytes_per_launch": b / n,
+                                "us_per_launch": 1e6 * t / n, "achieved_gbs": b / t / 1e9,
+                                "frac": b / t / 1e9 / hbm_peak}
+    flops_step = flops_per_sample(MODELS[args.model]) * args.microbatches * args.mbs * D
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         v, dt, cores = cpu_port_sample(desc)
@@ -434,14 +486,16 @@ def main():
                    "reference_peak_activation_units": [str(u) for u in wp.memory_profile(sim, sched)[1]]},
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05, all GEMM launches of the step)",
                      "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
-                     "frac": achieved / peak_tc if achieved else None, "traffic": traffic,
-                     "traffic_launch": traffic_info,
+                     "frac": achieved / peak_tc if achieved else None,
+                     "traffic": fc1["bytes_per_launch"] if fc1 else None, "traffic_launch": fc1,
                      "peak_kind": f"{peaks_kind} bf16 sustained (kernel timed inside a long step)",
                      "gemm_launches": g_launches, "gemm_share_of_step": g_sec / sec_prof},
         "attention": {"kernel": "flash_fwd_kernel / flash_bwd_kernel (tcgen05)", "launches": a_launches,
                       "achieved_tflops": a_flops / a_sec / 1e12 if a_sec > 0 else None,
                       "frac_of_peak": a_flops / a_sec / 1e12 / peak_tc if a_sec > 0 else None,
-                      "share_of_step": a_sec / sec_prof if sec_prof > 0 else None},
+                      "share_of_step": a_sec / sec_prof if sec_prof > 0 else None,
+                      "traffic_bwd_launch": attn_bwd_traffic},
+        "hbm": hbm,
         "cpu_baseline": cpu,
         "e2e": {"value": samples / sec_e2e, "unit": "samples/s",
                 "h2d_bytes_per_step": int(tok_h.numel() * 4 + lab_h.numel() * 4), "d2h_bytes_per_step": 4},

@@ -120,6 +120,16 @@ int wp_trace_build(int devices, const int* counts, const wp_interval* intervals,
  * wp_string_free. */
 int wp_trace_to_gantt(const wp_trace* trace, const char* format, char** out);
 
+/* compare + compare_to_csv / compare_to_json, src/analytics.cpp:221-331:
+ * n requests (scheme, waves) at a shared device budget and microbatch count,
+ * rows in ascending makespan; format 0 = CSV, 1 = JSON (the reference's
+ * bytes); *out freed with wp_string_free.  wp_compare_measured builds the
+ * same rows from measured traces (one per request, of lists[i]). */
+int wp_compare(const int* schemes, const int* waves, int n, int budget_devices, int microbatches,
+               const wp_cost* base_cost, int format, char** out);
+int wp_compare_measured(const int* schemes, const int* waves, int n, int budget_devices, int microbatches,
+                        const wp_trace* const* traces, const wp_list* const* lists, int format, char** out);
+
 /* bubble_ratio, src/analytics.cpp:32-46. */
 int wp_bubble_ratio(const wp_trace* trace, double* out);
 /* memory_profile, src/analytics.cpp:48-91: per device (num, den) pairs,
@@ -160,8 +170,6 @@ typedef struct wp_runtime wp_runtime;
  *  WP_TRANSPORT_LOCAL: every device of the list lives in this process;
  *    device d runs on CUDA ordinal device_ids[d] (ids may repeat: several
  *    pipeline devices sharing one GPU, each with its own streams).
- *  WP_TRANSPORT_NCCL: one process per pipeline device (rank == device);
- *    `nccl_id` is the 128-byte ncclUniqueId broadcast by the caller.
  *  WP_TRANSPORT_IPC: one process per GPU; messages are copy-engine pushes
  *    over NVLink into the receiver's CUDA-IPC-mapped landing slots,
  *    signalled by stream memory operations (no SMs spent on transfers).
@@ -173,12 +181,12 @@ typedef struct wp_runtime wp_runtime;
  *    kernel over NVLink.  After creation every rank exports
  *    wp_runtime_ipc_handle, the caller all-gathers the handles (rank order)
  *    and passes them to wp_runtime_ipc_connect before the first step.
- *    `nccl_id` is ignored. */
-enum { WP_TRANSPORT_LOCAL = 0, WP_TRANSPORT_NCCL = 1, WP_TRANSPORT_IPC = 2 };
+ *  (Value 1 is retired: the round-1 NCCL transport posted a step's receives
+ *  up front, beyond the reference's memory bound, and was removed.) */
+enum { WP_TRANSPORT_LOCAL = 0, WP_TRANSPORT_IPC = 2 };
 
 int wp_runtime_create(const wp_model_desc* model, const wp_list* list, int transport,
-                      const int* device_ids, int rank, const void* nccl_id,
-                      wp_runtime** out);
+                      const int* device_ids, int rank, wp_runtime** out);
 void wp_runtime_free(wp_runtime* rt);
 /* IPC transport handshake.  `out` receives WP_IPC_HANDLE_BYTES bytes;
  * `handles` holds nranks (= P * D) of them, rank-major. */
@@ -187,18 +195,30 @@ int wp_runtime_ipc_handle(wp_runtime* rt, void* out);
 int wp_runtime_ipc_connect(wp_runtime* rt, const void* handles, int nranks);
 /* After connect: *ok = 1 if every mapped peer accepted a probe copy and a
  * stream-memory-op write (the step's operations); else 0 and the reason in
- * `msg`, so all ranks can agree on another transport before stepping. */
+ * `msg` (the caller should stop: there is no other transport). */
 int wp_runtime_ipc_status(const wp_runtime* rt, int* ok, char* msg, int capacity);
-/* ncclGetUniqueId for rank 0 of a WP_TRANSPORT_NCCL job (128 bytes). */
-int wp_nccl_unique_id(void* out128);
 
 /* One synchronous training step (all microbatches, flush, optimizer).
  * tokens/labels: int32 [B * micro_batch_size * seq], microbatch-major, in HOST
  * or DEVICE memory (`on_device`).  *loss = mean loss over microbatches.
  * The measured trace (seconds, device clocks aligned) is available from
- * wp_runtime_trace until the next step. */
+ * wp_runtime_trace until the next step.
+ * Stream contract for device inputs: the runtime's streams wait for all work
+ * enqueued so far on the legacy default stream of the inputs' device (the
+ * stream PyTorch uses unless told otherwise); wp_train_step_stream names the
+ * producer stream (a cudaStream_t) explicitly.  Host inputs are read before
+ * the call returns.
+ * Stall watchdog (ref src/simulate.cpp:160-165): if the step's device work
+ * has not finished within the stall timeout (wp_runtime_set_stall_timeout,
+ * default 300 s or $WP_STALL_TIMEOUT_S) -- a dead, slow or mismatched peer
+ * rank -- the call returns WP_ERR_SEMANTIC naming the blocked action, after
+ * releasing this rank's pending device waits; the runtime then refuses
+ * further steps (free it). */
 int wp_train_step(wp_runtime* rt, const int32_t* tokens, const int32_t* labels, int on_device,
                   float* loss);
+int wp_train_step_stream(wp_runtime* rt, const int32_t* tokens, const int32_t* labels, int on_device,
+                         void* producer_stream, float* loss);
+int wp_runtime_set_stall_timeout(wp_runtime* rt, double seconds);
 int wp_runtime_trace(wp_runtime* rt, const wp_trace** trace);
 /* Enables per-action CUDA events (measured trace); off = no event overhead. */
 int wp_runtime_set_tracing(wp_runtime* rt, int enabled);
@@ -206,7 +226,7 @@ int wp_runtime_set_tracing(wp_runtime* rt, int enabled);
 int wp_runtime_set_update(wp_runtime* rt, int enabled);
 
 /* Parameter access by global name ("wte", "wpe", "h.<l>.ln1.w", ...), fp32.
- * Only the process owning the parameter can read it (NCCL transport). */
+ * Only the process owning the parameter can read it (IPC transport). */
 int wp_param_count(const wp_runtime* rt, int* count);
 int wp_param_info(const wp_runtime* rt, int index, const char** name, int64_t* numel, int* owned);
 int wp_get_param(wp_runtime* rt, const char* name, float* host_out, int64_t numel);
@@ -217,6 +237,13 @@ int wp_get_grad(wp_runtime* rt, const char* name, float* host_out, int64_t numel
  * message pool (grows to its steady state in the first step) and the IPC
  * landing slots (bytes). */
 int wp_runtime_memory(const wp_runtime* rt, int64_t* pool_bytes, int64_t* landing_bytes);
+/* Activation stash of local pipeline device `device` (the memory
+ * memory_profile counts, ref src/analytics.cpp:48-91): peak live bytes over
+ * the steps run so far, and per slice (nslices entries, normally
+ * config.stages) the bytes of one (microbatch, slice) entry -- the slice's
+ * input message plus every tensor its units saved for backward; 0 for
+ * slices on other devices. */
+int wp_runtime_stash(const wp_runtime* rt, int device, int64_t* peak_bytes, int64_t* slice_bytes, int nslices);
 /* Number of this library's kernels launched since the runtime was created. */
 int wp_runtime_launch_count(const wp_runtime* rt, int64_t* launches);
 /* GEMM profiling: CUDA events around every tcgen05/SIMT GEMM launch on its
@@ -228,6 +255,14 @@ int wp_runtime_gemm_stats(const wp_runtime* rt, int64_t* launches, double* flops
 int wp_runtime_attn_stats(const wp_runtime* rt, int64_t* launches, double* flops, double* seconds);
 /* Text table of the profiled GEMMs by shape (launches, time, TFLOP/s). */
 int wp_runtime_gemm_report(const wp_runtime* rt, char* buf, int capacity);
+/* The HBM-bound kernels timed the same way, by kernel class ("layernorm_fwd",
+ * "layernorm_bwd_dx", "cross_entropy", "embedding_fwd", "embedding_bwd",
+ * "optimizer", ...): count of classes, then per class its launches,
+ * algorithmic bytes (reads + writes of the tensors it must touch) and summed
+ * kernel seconds.  `name` stays valid until profiling is re-enabled. */
+int wp_runtime_hbm_count(const wp_runtime* rt, int* classes);
+int wp_runtime_hbm_stat(const wp_runtime* rt, int index, const char** name, int64_t* launches, double* bytes,
+                        double* seconds);
 
 #ifdef __cplusplus
 }

@@ -281,6 +281,42 @@ MetricsReport compute_metrics(const SimTrace& trace, const ActionList& list);
 std::string metrics_to_text(const MetricsReport& report);
 std::string metrics_to_json(const MetricsReport& report);
 
+// Scheme comparison sweep (ref include/wavepipe/analytics.hpp:104-140,
+// src/analytics.cpp:221-331): every request evaluated at one device budget
+// and total microbatch count (chimera-wave as one of its two symmetric
+// device groups: half the budget and microbatches, costs rescaled), rows in
+// ascending makespan; failures are captured per row and sort last.
+struct CompareRequest {
+  Scheme scheme = Scheme::GPipe;
+  int waves = 1;
+};
+struct CompareRow {
+  Scheme scheme = Scheme::GPipe;
+  int devices = 0;       // shared device budget
+  int microbatches = 0;  // total microbatches
+  int waves = 1;
+  double makespan = 0.0;
+  double simulated_ratio = 0.0;
+  bool has_analytic = false;
+  double analytic_ratio = 0.0;
+  Rational weight_units;     // per device (max over devices)
+  Rational peak_activation;  // max across devices
+  Rational variance;
+  bool failed = false;
+  std::string error;
+};
+std::vector<CompareRow> compare(const std::vector<CompareRequest>& requests, int budget_devices, int microbatches,
+                                const CostModel& base_cost);
+// The same rows from MEASURED traces (the GPU runtime's train_step, one per
+// request, traces[i] of lists[i]): makespan = measured step (seconds),
+// simulated_ratio = bubble_ratio of the measured trace; Hanayo's analytic
+// ratio at the measured mean slice costs.  Same order and writers.
+std::vector<CompareRow> compare_measured(const std::vector<CompareRequest>& requests, int budget_devices,
+                                         int microbatches, const std::vector<SimTrace>& traces,
+                                         const std::vector<ActionList>& lists);
+std::string compare_to_csv(const std::vector<CompareRow>& rows);
+std::string compare_to_json(const std::vector<CompareRow>& rows);
+
 // ---------------------------------------------------------------------------
 // Action-list JSON (ref include/wavepipe/serialize.hpp:26-47): stock
 // nlohmann-style `dump(2)` bytes, strict parser.

@@ -37,7 +37,6 @@ struct ModelSpec {
 
 enum class Transport {
   Local = 0,  // every pipeline device of the list in this process
-  Nccl = 1,   // one process per GPU, NCCL send/recv
   Ipc = 2,    // one process per GPU, copy-engine pushes into CUDA-IPC landing slots
 };
 
@@ -51,9 +50,9 @@ struct Batch {
 class Runtime {
  public:
   // device_ids: CUDA ordinal per pipeline device (Local) or this rank's GPU
-  // (Nccl / Ipc); rank: pipeline device (Nccl) or replica * P + device (Ipc).
+  // (Ipc); rank: replica * P + pipeline device (Ipc).
   Runtime(const ModelSpec& model, const ActionList& list, Transport transport = Transport::Local,
-          std::vector<int> device_ids = {}, int rank = 0, const void* nccl_id = nullptr);
+          std::vector<int> device_ids = {}, int rank = 0);
   ~Runtime();
   Runtime(const Runtime&) = delete;
   Runtime& operator=(const Runtime&) = delete;

@@ -135,6 +135,24 @@ int main(int argc, char** argv) {
                                                       std::atof(argv[6])));
       return 0;
     }
+    if (cmd == "compare" && argc >= 9) {  // compare P B tf tb tc csv|json scheme:waves...
+      std::vector<CompareRequest> reqs;
+      for (int i = 8; i < argc; ++i) {
+        std::string a = argv[i];
+        const size_t colon = a.find(':');
+        CompareRequest r;
+        r.scheme = parse_scheme(a.substr(0, colon).c_str());
+        r.waves = colon == std::string::npos ? 1 : std::atoi(a.c_str() + colon + 1);
+        reqs.push_back(r);
+      }
+      CostModel cost;
+      cost.t_forward = std::atof(argv[4]);
+      cost.t_backward = std::atof(argv[5]);
+      cost.t_comm = std::atof(argv[6]);
+      const auto rows = compare(reqs, std::atoi(argv[2]), std::atoi(argv[3]), cost);
+      std::fputs((std::string(argv[7]) == "csv" ? compare_to_csv(rows) : compare_to_json(rows)).c_str(), stdout);
+      return 0;
+    }
     if (cmd == "time" && argc == 7) {
       ScheduleConfig cfg = make_config(parse_scheme(argv[2]), std::atoi(argv[3]),
                                        std::atoi(argv[4]), std::atoi(argv[5]), 1);

@@ -6,4 +6,4 @@ C ABI of libwavepipe.so (include/wavepipe.h); there is no Python fallback.
 """
 from . import schedule  # noqa: F401
 from .schedule import *  # noqa: F401,F403
-from .runtime import ModelDesc, Runtime, TRANSPORT_IPC, TRANSPORT_LOCAL, TRANSPORT_NCCL  # noqa: F401,E402
+from .runtime import ModelDesc, Runtime, TRANSPORT_IPC, TRANSPORT_LOCAL  # noqa: F401,E402

@@ -85,18 +85,22 @@ _SIGS = {
     "wp_trace_free": (None, [P]),
     "wp_trace_build": (I, [I, IP, C.POINTER(wp_interval), I, C.POINTER(wp_comm_event), PP]),
     "wp_trace_to_gantt": (I, [P, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "wp_compare": (I, [IP, IP, I, I, I, C.POINTER(wp_cost), I, C.POINTER(C.c_void_p)]),
+    "wp_compare_measured": (I, [IP, IP, I, I, I, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), I,
+                                C.POINTER(C.c_void_p)]),
     "wp_bubble_ratio": (I, [P, DP]),
     "wp_memory_profile": (I, [P, P, I64P, I64P]),
     "wp_analytic_bubble": (I, [I, I, D, D, D, DP]),
     "wp_analytic_bubble_exact": (I, [I, I, I64P, I64P, I64P, I64P]),
     "wp_analytic_bubble_simplified": (I, [I, I, I64P]),
-    "wp_runtime_create": (I, [C.POINTER(wp_model_desc), P, I, IP, I, C.c_void_p, PP]),
+    "wp_runtime_create": (I, [C.POINTER(wp_model_desc), P, I, IP, I, PP]),
     "wp_runtime_free": (None, [P]),
-    "wp_nccl_unique_id": (I, [C.c_void_p]),
     "wp_runtime_ipc_handle": (I, [P, C.c_void_p]),
     "wp_runtime_ipc_connect": (I, [P, C.c_void_p, I]),
     "wp_runtime_ipc_status": (I, [P, IP, C.c_char_p, I]),
     "wp_train_step": (I, [P, C.c_void_p, C.c_void_p, I, C.POINTER(C.c_float)]),
+    "wp_train_step_stream": (I, [P, C.c_void_p, C.c_void_p, I, C.c_void_p, C.POINTER(C.c_float)]),
+    "wp_runtime_set_stall_timeout": (I, [P, D]),
     "wp_runtime_trace": (I, [P, PP]),
     "wp_runtime_set_tracing": (I, [P, I]),
     "wp_runtime_set_update": (I, [P, I]),
@@ -107,10 +111,13 @@ _SIGS = {
     "wp_get_grad": (I, [P, C.c_char_p, C.POINTER(C.c_float), C.c_int64]),
     "wp_runtime_launch_count": (I, [P, I64P]),
     "wp_runtime_memory": (I, [P, I64P, I64P]),
+    "wp_runtime_stash": (I, [P, I, I64P, I64P, I]),
     "wp_runtime_set_profiling": (I, [P, I]),
     "wp_runtime_gemm_stats": (I, [P, I64P, DP, DP]),
     "wp_runtime_gemm_report": (I, [P, C.c_char_p, I]),
     "wp_runtime_attn_stats": (I, [P, I64P, DP, DP]),
+    "wp_runtime_hbm_count": (I, [P, IP]),
+    "wp_runtime_hbm_stat": (I, [P, I, C.POINTER(C.c_char_p), I64P, DP, DP]),
 }
 
 EXPORTED = tuple(_SIGS)

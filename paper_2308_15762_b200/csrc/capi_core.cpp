@@ -211,6 +211,58 @@ int wp_serialize(const wp_list* l, char** json) {
   }
 }
 
+namespace {
+char* dup_c(const std::string& s) {
+  char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return buf;
+}
+std::vector<wavepipe::CompareRequest> requests_of(const int* schemes, const int* waves, int n) {
+  std::vector<wavepipe::CompareRequest> r(n);
+  for (int i = 0; i < n; ++i) {
+    if (schemes[i] < 0 || schemes[i] > static_cast<int>(wavepipe::Scheme::Hanayo)) {
+      throw wavepipe::ConfigError("compare: unknown scheme " + std::to_string(schemes[i]));
+    }
+    r[i].scheme = static_cast<wavepipe::Scheme>(schemes[i]);
+    r[i].waves = waves[i];
+  }
+  return r;
+}
+}  // namespace
+
+int wp_compare(const int* schemes, const int* waves, int n, int budget_devices, int microbatches,
+               const wp_cost* base_cost, int format, char** out) {
+  try {
+    if ((n > 0 && (!schemes || !waves)) || !base_cost || !out) return fail(WP_ERR_CONFIG, "null argument");
+    wavepipe::CostModel c;
+    c.t_forward = base_cost->t_forward, c.t_backward = base_cost->t_backward, c.t_comm = base_cost->t_comm;
+    const auto rows = wavepipe::compare(requests_of(schemes, waves, n), budget_devices, microbatches, c);
+    *out = dup_c(format == 1 ? wavepipe::compare_to_json(rows) : wavepipe::compare_to_csv(rows));
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int wp_compare_measured(const int* schemes, const int* waves, int n, int budget_devices, int microbatches,
+                        const wp_trace* const* traces, const wp_list* const* lists, int format, char** out) {
+  try {
+    if ((n > 0 && (!schemes || !waves || !traces || !lists)) || !out) return fail(WP_ERR_CONFIG, "null argument");
+    std::vector<wavepipe::SimTrace> tr;
+    std::vector<wavepipe::ActionList> ls;
+    for (int i = 0; i < n; ++i) {
+      if (!traces[i] || !lists[i]) return fail(WP_ERR_CONFIG, "null trace or list");
+      tr.push_back(traces[i]->trace);
+      ls.push_back(lists[i]->list);
+    }
+    const auto rows = wavepipe::compare_measured(requests_of(schemes, waves, n), budget_devices, microbatches, tr, ls);
+    *out = dup_c(format == 1 ? wavepipe::compare_to_json(rows) : wavepipe::compare_to_csv(rows));
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 int wp_trace_to_gantt(const wp_trace* t, const char* format, char** out) {
   try {
     if (!t || !format || !out) return fail(WP_ERR_CONFIG, "null argument");

@@ -7,7 +7,6 @@
 #include <memory>
 
 #include "capi_internal.hpp"
-#include "runtime/nccl_shim.hpp"
 #include "runtime/runtime.hpp"
 
 struct wp_runtime {
@@ -21,7 +20,7 @@ using wpc::map_exception;
 extern "C" {
 
 int wp_runtime_create(const wp_model_desc* model, const wp_list* list, int transport, const int* device_ids,
-                      int rank, const void* nccl_id, wp_runtime** out) {
+                      int rank, wp_runtime** out) {
   try {
     if (!model || !list || !out) return fail(WP_ERR_CONFIG, "null argument");
     int n = 0;
@@ -31,7 +30,7 @@ int wp_runtime_create(const wp_model_desc* model, const wp_list* list, int trans
     }
     auto* r = new wp_runtime;
     try {
-      r->rt = std::make_unique<wprt::Runtime>(*model, list->list, transport, device_ids, rank, nccl_id);
+      r->rt = std::make_unique<wprt::Runtime>(*model, list->list, transport, device_ids, rank);
     } catch (...) {
       delete r;
       throw;
@@ -77,6 +76,16 @@ int wp_runtime_memory(const wp_runtime* rt, int64_t* pool_bytes, int64_t* landin
   return WP_OK;
 }
 
+int wp_runtime_stash(const wp_runtime* rt, int device, int64_t* peak_bytes, int64_t* slice_bytes, int nslices) {
+  try {
+    if (!rt || !peak_bytes || (nslices > 0 && !slice_bytes)) return fail(WP_ERR_CONFIG, "null argument");
+    rt->rt->stash_stats(device, peak_bytes, slice_bytes, nslices);
+    return WP_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 int wp_runtime_ipc_status(const wp_runtime* rt, int* ok, char* msg, int capacity) {
   if (!rt || !ok) return fail(WP_ERR_CONFIG, "null argument");
   *ok = rt->rt->ipc_ok() ? 1 : 0;
@@ -89,30 +98,42 @@ int wp_runtime_ipc_status(const wp_runtime* rt, int* ok, char* msg, int capacity
   return WP_OK;
 }
 
-int wp_nccl_unique_id(void* out128) {
-  if (!out128) return fail(WP_ERR_CONFIG, "null argument");
-  ncclUniqueId id;
-  try {
-    const auto& api = wprt::NcclApi::get();
-    const ncclResult_t r = api.GetUniqueId(&id);
-    if (r != ncclSuccess) return fail(WP_ERR_CUDA, std::string("ncclGetUniqueId: ") + api.GetErrorString(r));
-  } catch (const std::exception& e) {
-    return fail(WP_ERR_CUDA, e.what());
-  }
-  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
-  std::memcpy(out128, &id, sizeof(id));
-  return WP_OK;
-}
-
-int wp_train_step(wp_runtime* rt, const int32_t* tokens, const int32_t* labels, int on_device, float* loss) {
+int wp_train_step_stream(wp_runtime* rt, const int32_t* tokens, const int32_t* labels, int on_device,
+                         void* producer_stream, float* loss) {
   try {
     if (!rt || !tokens || !labels) return fail(WP_ERR_CONFIG, "null argument");
-    const float l = rt->rt->train_step(tokens, labels, on_device != 0);
+    const float l =
+        rt->rt->train_step(tokens, labels, on_device != 0, static_cast<cudaStream_t>(producer_stream));
     if (loss) *loss = l;
     return WP_OK;
   } catch (...) {
     return map_exception();
   }
+}
+
+int wp_train_step(wp_runtime* rt, const int32_t* tokens, const int32_t* labels, int on_device, float* loss) {
+  return wp_train_step_stream(rt, tokens, labels, on_device, nullptr, loss);
+}
+
+int wp_runtime_set_stall_timeout(wp_runtime* rt, double seconds) {
+  if (!rt) return fail(WP_ERR_CONFIG, "null argument");
+  if (!(seconds > 0)) return fail(WP_ERR_CONFIG, "stall timeout must be positive");
+  rt->rt->set_stall_timeout(seconds);
+  return WP_OK;
+}
+
+int wp_runtime_hbm_count(const wp_runtime* rt, int* classes) {
+  if (!rt || !classes) return fail(WP_ERR_CONFIG, "null argument");
+  *classes = rt->rt->hbm_count();
+  return WP_OK;
+}
+
+int wp_runtime_hbm_stat(const wp_runtime* rt, int index, const char** name, int64_t* launches, double* bytes,
+                        double* seconds) {
+  if (!rt || !name || !launches || !bytes || !seconds) return fail(WP_ERR_CONFIG, "null argument");
+  if (index < 0 || index >= rt->rt->hbm_count()) return fail(WP_ERR_CONFIG, "hbm class index out of range");
+  rt->rt->hbm_stat(index, name, launches, bytes, seconds);
+  return WP_OK;
 }
 
 int wp_runtime_trace(wp_runtime* rt, const wp_trace** trace) {

@@ -838,13 +838,16 @@ int ln_fwd_dispatch(const T* x, const float* w, const float* b, T* y, float* mea
       return 1;
     }
   }
+  // One instantiation per chunk count: every hidden size ModelSpec accepts
+  // (a multiple of 256 up to 4096).
   switch (h / 256) {
-    case 1: ln_fwd_k<T, 1><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
-    case 2: ln_fwd_k<T, 2><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
-    case 4: ln_fwd_k<T, 4><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
-    case 8: ln_fwd_k<T, 8><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
-    case 16: ln_fwd_k<T, 16><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
-    default: throw std::runtime_error("layernorm: hidden must be 256 * {1,2,4,8,16}");
+#define WP_LN_FWD_CASE(c) \
+  case c: ln_fwd_k<T, c><<<grid, block, 0, s>>>(x, w, b, y, mean, rstd, T_, h); break;
+    WP_LN_FWD_CASE(1) WP_LN_FWD_CASE(2) WP_LN_FWD_CASE(3) WP_LN_FWD_CASE(4) WP_LN_FWD_CASE(5) WP_LN_FWD_CASE(6)
+    WP_LN_FWD_CASE(7) WP_LN_FWD_CASE(8) WP_LN_FWD_CASE(9) WP_LN_FWD_CASE(10) WP_LN_FWD_CASE(11)
+    WP_LN_FWD_CASE(12) WP_LN_FWD_CASE(13) WP_LN_FWD_CASE(14) WP_LN_FWD_CASE(15) WP_LN_FWD_CASE(16)
+#undef WP_LN_FWD_CASE
+    default: throw std::runtime_error("layernorm: hidden must be a multiple of 256, at most 4096");
   }
   check_launch("layernorm_fwd");
   return 1;
@@ -911,6 +914,17 @@ int ln_bwd_dispatch(const T* dy, const T* x, const float* mean, const float* rst
   check_launch("layernorm_bwd_dwdb");
   return 2;
 }
+
+__global__ void wait_flag_k(const uint32_t* flag, uint32_t epoch, const volatile uint32_t* abort_word) {
+  for (uint32_t it = 0;; ++it) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (static_cast<int32_t>(v - epoch) >= 0) return;
+    if ((it & 15) == 15 && *abort_word) return;  // host memory: polled every 16th spin
+    __nanosleep(256);
+  }
+}
+
 
 // One-shot all-reduce (scaled sum) of this member's share; float4 granules,
 // fixed summation order (member 0..G-1) so every member stores the same bits.
@@ -1024,6 +1038,12 @@ int softmax_bwd(int dtype, const float* dP, void* P, int rows, int n, float scal
   if (dtype == kBF16) softmax_bwd_k<bf16><<<grid, 256, 0, s>>>(dP, static_cast<bf16*>(P), rows, n, scale, causal);
   else softmax_bwd_k<float><<<grid, 256, 0, s>>>(dP, static_cast<float*>(P), rows, n, scale, causal);
   check_launch("softmax_bwd");
+  return 1;
+}
+
+int wait_flag(cudaStream_t s, const uint32_t* flag, uint32_t epoch, const uint32_t* abort_word) {
+  wait_flag_k<<<1, 1, 0, s>>>(flag, epoch, abort_word);
+  check_launch("wait_flag");
   return 1;
 }
 

@@ -67,6 +67,13 @@ int optimizer_step(const OptimArgs& a, float* master, float* grad, float* m, flo
 // stores the result into every buffer.
 int allreduce_scaled_peers(float* const* bufs, int G, int me, int64_t n, float scale, cudaStream_t s);
 
+// Bounded device-side wait of the IPC transport: the stream proceeds once
+// *flag >= epoch (wrap-free, like CU_STREAM_WAIT_VALUE_GEQ) -- the flag
+// written by a peer's stream memory op -- or once the host sets *abort
+// (mapped pinned memory: the stall watchdog's release).  One thread; the
+// acquire load at system scope orders the peer's bytes before what follows.
+int wait_flag(cudaStream_t s, const uint32_t* flag, uint32_t epoch, const uint32_t* abort_word);
+
 // Deterministic N(0, std) init from a counter-based hash (Box-Muller).
 int init_normal(float* p, int64_t n, float std, uint64_t seed, cudaStream_t s);
 int fill_f32(float* p, int64_t n, float v, cudaStream_t s);

@@ -33,9 +33,9 @@ int64_t signature(const ActionList& l) {
 }  // namespace
 
 Runtime::Runtime(const ModelSpec& model, const ActionList& list, Transport transport, std::vector<int> device_ids,
-                 int rank, const void* nccl_id)
+                 int rank)
     : impl_(std::make_unique<wprt::Runtime>(to_desc(model), list, static_cast<int>(transport),
-                                            device_ids.empty() ? nullptr : device_ids.data(), rank, nccl_id)),
+                                            device_ids.empty() ? nullptr : device_ids.data(), rank)),
       list_signature_(signature(list)) {}
 
 Runtime::~Runtime() = default;

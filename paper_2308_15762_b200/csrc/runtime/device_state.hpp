@@ -12,7 +12,6 @@
 #include <vector>
 
 #include "capi_internal.hpp"
-#include "runtime/nccl_shim.hpp"
 #include "runtime/runtime.hpp"
 
 namespace wprt {
@@ -21,9 +20,6 @@ using wavepipe::ActionKind;
 
 inline void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw wpc::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
-}
-inline void ckn(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) throw wpc::CudaError(std::string(what) + ": " + NcclApi::get().GetErrorString(r));
 }
 
 struct DevGuard {
@@ -52,6 +48,13 @@ struct DeviceState {
   float* dq_acc = nullptr;      // fp32 [T, h]             (fused attention backward)
   float* ln_rows = nullptr;     // fp32 [T, 2]  LayerNorm-backward row sums (GEMM-fused path)
   int bwd_unit_lo = 0;          // first unit of the slice being run backward
+  // Activation stash accounting (ref src/analytics.cpp:61-76): bytes held by
+  // live (microbatch, slice) stash entries -- the slice's input message and
+  // every tensor its units saved -- added when the forward is enqueued,
+  // removed when its backward is; the high-water mark over all steps, and
+  // per slice the largest entry seen.
+  int64_t live_stash = 0, peak_stash = 0;
+  std::map<int, int64_t> slice_stash_bytes;
   bool dy_bias_done = false;    // the incoming dy's column sums are already in this unit's bias grad
   std::vector<std::pair<int, int>> be_partner;  // per position: (device, position) of a BE's counterpart
 
@@ -66,10 +69,11 @@ struct DeviceState {
   std::vector<cudaEvent_t> events;
   size_t ev_next = 0;
   std::vector<uint8_t> published_at;  // BE positions whose outgoing message is published
-  // NCCL transport: per-peer send / receive streams and the step's posted
-  // receives (landing buffer + arrival event per message).
-  std::map<int, cudaStream_t> tx, rx;
-  std::map<MsgKey, std::pair<BufPtr, cudaEvent_t>> posted;
+  // IPC transport: per-peer outgoing copy streams.
+  std::map<int, cudaStream_t> tx;
+  // Start event of every compute enqueued this step (program position,
+  // event): the watchdog names the first one that never started.
+  std::vector<std::pair<size_t, cudaEvent_t>> starts;
   // IPC transport: messages whose landing slot the next compute copies out
   // (after its arrival flag reaches the step epoch), and the stream that
   // writes "posted" flags into senders' arenas.
@@ -95,6 +99,7 @@ struct DeviceState {
     cudaEvent_t s, e;
     std::string shape;
     bool attention = false;  // fused attention launch (reported apart from the GEMMs)
+    bool hbm = false;        // HBM-bound kernel class (`shape` = class name, `flops` = bytes)
   };
   std::vector<GemmRec> gemm_recs;
 };

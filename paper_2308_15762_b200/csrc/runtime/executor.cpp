@@ -3,17 +3,18 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
+#include <thread>
 
 #include "capi_internal.hpp"
 #include "kernels/attention.cuh"
 #include "runtime/device_state.hpp"
-#include "runtime/nccl_shim.hpp"
 #include "runtime/runtime.hpp"
 #include "runtime/stream_ops.hpp"
 
@@ -38,6 +39,7 @@ uint64_t name_hash(const std::string& s) {
 
 // --------------------------------------------------------------------- pool
 Pool::~Pool() {
+  if (leak_) return;
   DevGuard g(dev_);
   for (auto& b : all_) {
     if (b->p) cudaFree(b->p);
@@ -98,7 +100,7 @@ void Pool::release(const BufPtr& b, cudaStream_t stream) {
 
 // ------------------------------------------------------------------ runtime
 Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, int transport, const int* device_ids,
-                 int rank, const void* nccl_id)
+                 int rank)
     : m_(ModelSpec::from_desc(desc)), list_(list), transport_(transport), rank_(rank) {
   // IPC transport: `rank` is the global rank replica * P + pipeline device.
   replicas_ = std::max(1, list_.config.replicas);
@@ -122,7 +124,6 @@ Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, in
       for (const auto& sl : list_.placement.assignment[d]) slice_device[sl.index] = d;
     bounds_ = partition_units(units_, slice_device, list_.config.devices);
   }
-  const int P = list_.config.devices;
   if (m_.tie) {  // every device holding the embedding slice also holds the head slice (Hanayo, Chimera)
     for (const auto& dev : list_.placement.assignment) {
       bool first = false, last = false;
@@ -138,85 +139,33 @@ Runtime::Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, in
         "Chimera holds every stage on two devices (p and P-1-p) that sum their gradients over peer memory: "
         "it needs the IPC transport (one process per device)");
   }
-  if (transport_ != WP_TRANSPORT_LOCAL && transport_ != WP_TRANSPORT_NCCL && transport_ != WP_TRANSPORT_IPC) {
-    throw wavepipe::ConfigError("unknown transport");
+  if (transport_ != WP_TRANSPORT_LOCAL && transport_ != WP_TRANSPORT_IPC) {
+    throw wavepipe::ConfigError(transport_ == 1 ? "transport 1 (NCCL) was removed: use WP_TRANSPORT_IPC"
+                                                : "unknown transport");
   }
-  if (transport_ == WP_TRANSPORT_NCCL && (rank_ < 0 || rank_ >= P || !nccl_id)) {
-    throw wavepipe::ConfigError("NCCL transport needs 0 <= rank < P and an ncclUniqueId");
+  if (const char* t = std::getenv("WP_STALL_TIMEOUT_S")) {
+    const double v = std::atof(t);
+    if (v > 0) stall_timeout_s_ = v;
   }
   build_devices(device_ids);
-  if (transport_ == WP_TRANSPORT_NCCL) {
-    ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof(id));
-    DevGuard g(devs_[0]->cuda);
-    ncclComm_t comm;
-    ckn(NcclApi::get().CommInitRank(&comm, P, id, rank_), "ncclCommInitRank");
-    nccl_comm_ = comm;
-    build_channels();
-  }
   if (transport_ == WP_TRANSPORT_IPC) ipc_setup();
 }
 
-void Runtime::build_channels() {
-  // Sender-order message lists per directed pair, from the full list every
-  // rank holds; then one ncclCommSplit per pair, called by every rank in the
-  // same order (collective), members keyed sender=0 / receiver=1.
-  std::map<std::pair<int, int>, std::vector<MsgKey>> plan;
-  for (int p = 0; p < list_.config.devices; ++p)
-    for (const Action& a : list_.per_device[p])
-      if (a.kind == ActionKind::Send || a.kind == ActionKind::BatchedExchange) plan[{p, a.peer}].push_back(message_key(a));
-  DeviceState& d = *devs_[0];
-  DevGuard g(d.cuda);
-  for (auto& [pair, keys] : plan) {
-    Channel c;
-    c.src = pair.first;
-    c.dst = pair.second;
-    c.keys = keys;
-    const bool member = rank_ == c.src || rank_ == c.dst;
-    ncclComm_t sub = nullptr;
-    ckn(NcclApi::get().CommSplit(static_cast<ncclComm_t>(nccl_comm_), member ? static_cast<int>(channels_.size()) : -1,
-                                 rank_ == c.src ? 0 : 1, &sub, nullptr),
-        "ncclCommSplit");
-    c.comm = sub;
-    if (rank_ == c.src && !d.tx.count(c.dst)) {
-      cudaStream_t s;
-      ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-      d.tx[c.dst] = s;
-    }
-    if (rank_ == c.dst && !d.rx.count(c.src)) {
-      cudaStream_t s;
-      ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-      d.rx[c.src] = s;
-    }
-    channels_.push_back(c);
-  }
-}
-
-void Runtime::post_channel_receives(DeviceState& d) {
-  // Every incoming message of the step, per channel in the sender's order:
-  // NCCL matches a pair's messages FIFO, so posting in sender order gives
-  // each message its own landing buffer whatever order this device consumes
-  // them in.  Receives wait on nothing but earlier receives of the channel.
-  const size_t bytes = size_t(m_.tokens()) * m_.hidden * m_.act_bytes();
-  for (const Channel& c : channels_) {
-    if (c.dst != d.pipe) continue;
-    cudaStream_t s = d.rx.at(c.src);
-    ck(cudaStreamWaitEvent(s, d.step_begin, 0), "rx after begin");
-    for (const MsgKey& k : c.keys) {
-      BufPtr landing = d.pool->alloc(bytes, s, 1);
-      ckn(NcclApi::get().Recv(landing->p, bytes, ncclUint8, 0, static_cast<ncclComm_t>(c.comm), s), "ncclRecv");
-      cudaEvent_t arrive = next_event(d);
-      ck(cudaEventRecord(arrive, s), "record arrival");
-      d.posted[k] = {landing, arrive};
-    }
-  }
-}
-
 Runtime::~Runtime() {
+  if (broken_ && !released_) {
+    // A stalled step whose device waits could not be released: the streams
+    // stay blocked until the process exits, and every freeing call below
+    // (cudaFree, cudaDeviceSynchronize) would block with them.  Leak the
+    // device state instead; the driver reclaims it at process exit.
+    for (auto& d : devs_) d->pool->leak();
+    for (auto& d : devs_) d.release();
+    return;
+  }
   ipc_release();
-  for (auto& c : channels_)
-    if (c.comm) NcclApi::get().CommDestroy(static_cast<ncclComm_t>(c.comm));
-  if (nccl_comm_) NcclApi::get().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
+  if (input_ready_) {
+    DevGuard g(input_ready_dev_);
+    cudaEventDestroy(input_ready_);
+  }
   for (auto& d : devs_) {
     DevGuard g(d->cuda);
     cudaDeviceSynchronize();
@@ -232,7 +181,6 @@ Runtime::~Runtime() {
     if (d->compute) cudaStreamDestroy(d->compute);
     if (d->copy) cudaStreamDestroy(d->copy);
     for (auto& kv : d->tx) cudaStreamDestroy(kv.second);
-    for (auto& kv : d->rx) cudaStreamDestroy(kv.second);
   }
 }
 
@@ -632,6 +580,21 @@ void Runtime::timed_attention(DeviceState& d, bool backward, F&& launch) {
                          true});
 }
 
+template <typename F>
+void Runtime::timed_hbm(DeviceState& d, const char* cls, double bytes, F&& launch) {
+  if (!profiling_) {
+    launch();
+    return;
+  }
+  cudaEvent_t s = next_event(d), e = next_event(d);
+  ck(cudaEventRecord(s, d.compute), "record hbm start");
+  launch();
+  ck(cudaEventRecord(e, d.compute), "record hbm end");
+  DeviceState::GemmRec r{bytes, s, e, cls};
+  r.hbm = true;
+  d.gemm_recs.push_back(r);
+}
+
 bool Runtime::use_flash() const {
   static const bool off = std::getenv("WP_NO_FLASH") != nullptr;
   return !off && m_.dtype == wpk::kBF16 && wpk::flash_supported(attn_shape());
@@ -674,8 +637,11 @@ BufPtr Runtime::unit_fwd(DeviceState& d, int ui, int mb, BufPtr x, UnitStash& st
 
   if (u.kind == UnitKind::Embed) {
     BufPtr out = act(int64_t(T) * h);
-    launches_ += wpk::embed_fwd(dt, d.tokens + int64_t(mb) * T, weight(d, "wte"), weight(d, "wpe"), out->p, T, S, h,
-                                cs);
+    // tokens, the T gathered wte rows, the wpe table, the output
+    timed_hbm(d, "embedding_fwd", 4.0 * T + double(es) * (2.0 * T * h + double(S) * h), [&] {
+      launches_ += wpk::embed_fwd(dt, d.tokens + int64_t(mb) * T, weight(d, "wte"), weight(d, "wpe"), out->p, T, S,
+                                  h, cs);
+    });
     return out;
   }
   st.x = x;
@@ -684,8 +650,11 @@ BufPtr Runtime::unit_fwd(DeviceState& d, int ui, int mb, BufPtr x, UnitStash& st
   st.rstd = f32(T);
   const char* lnw = u.kind == UnitKind::Attn ? "ln1" : u.kind == UnitKind::Mlp ? "ln2" : nullptr;
   const std::string lnname = u.kind == UnitKind::Head ? "lnf" : L + lnw;
-  launches_ += wpk::layernorm_fwd(dt, x->p, master(d, lnname + ".w"), master(d, lnname + ".b"), st.ln->p,
-                                  static_cast<float*>(st.mean->p), static_cast<float*>(st.rstd->p), T, h, cs);
+  // x in, y out, mean / rstd out, w / b in
+  timed_hbm(d, "layernorm_fwd", 2.0 * es * T * h + 8.0 * T + 8.0 * h, [&] {
+    launches_ += wpk::layernorm_fwd(dt, x->p, master(d, lnname + ".w"), master(d, lnname + ".b"), st.ln->p,
+                                    static_cast<float*>(st.mean->p), static_cast<float*>(st.rstd->p), T, h, cs);
+  });
   if (check_ops_enabled())
     check_layernorm(dt, x->p, master(d, lnname + ".w"), master(d, lnname + ".b"), st.ln->p,
                     static_cast<float*>(st.mean->p), static_cast<float*>(st.rstd->p), T, h, cs);
@@ -769,7 +738,10 @@ BufPtr Runtime::unit_fwd(DeviceState& d, int ui, int mb, BufPtr x, UnitStash& st
   g.epi.c = st.a->p, g.epi.c_dtype = dt, g.epi.ldc = V;
   gemm(d, g);
   const float scale = 1.0f / (static_cast<float>(T) * list_.config.microbatches);
-  launches_ += wpk::xent_fwd_bwd(dt, st.a->p, d.labels + int64_t(mb) * T, d.loss, T, V, scale, scale, cs);
+  // logits read once, dlogits written in place, labels
+  timed_hbm(d, "cross_entropy", 2.0 * es * T * double(V) + 4.0 * T, [&] {
+    launches_ += wpk::xent_fwd_bwd(dt, st.a->p, d.labels + int64_t(mb) * T, d.loss, T, V, scale, scale, cs);
+  });
   return nullptr;
 }
 
@@ -789,7 +761,12 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   d.dy_bias_done = false;
 
   if (u.kind == UnitKind::Embed) {
-    launches_ += wpk::embed_bwd(dt, d.tokens + int64_t(mb) * T, dy->p, grad(d, "wte"), grad(d, "wpe"), T, S, h, cs);
+    // dy and tokens in; the T touched fp32 wte-gradient rows and the wpe
+    // gradient read-modify-written
+    timed_hbm(d, "embedding_bwd", double(es) * T * h + 4.0 * T + 8.0 * (double(T) * h + double(S) * h), [&] {
+      launches_ += wpk::embed_bwd(dt, d.tokens + int64_t(mb) * T, dy->p, grad(d, "wte"), grad(d, "wpe"), T, S, h,
+                                  cs);
+    });
     drop(dy);
     return nullptr;
   }
@@ -857,9 +834,13 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     BufPtr dx = act(int64_t(T) * h);
     if (ln_fused) {  // dw, db, row sums came with dLN from the dgrad GEMM
       float* dcol = below_bias();
-      launches_ += wpk::layernorm_bwd_dx_rows(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p),
-                                              static_cast<float*>(st.rstd->p), master(d, name + ".w"), d.ln_rows,
-                                              dres ? dres->p : nullptr, dx->p, T, h, cs, dcol);
+      // dLN, x, (dres) in, dx out; mean, rstd, two row sums; w; bias-sum RMW
+      const double bytes = double(es) * T * h * (dres ? 4.0 : 3.0) + 16.0 * T + 4.0 * h + (dcol ? 8.0 * h : 0.0);
+      timed_hbm(d, "layernorm_bwd_dx", bytes, [&] {
+        launches_ += wpk::layernorm_bwd_dx_rows(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p),
+                                                static_cast<float*>(st.rstd->p), master(d, name + ".w"), d.ln_rows,
+                                                dres ? dres->p : nullptr, dx->p, T, h, cs, dcol);
+      });
       d.dy_bias_done = dcol != nullptr;
       return dx;
     }
@@ -868,10 +849,12 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
       chk.before(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p), static_cast<float*>(st.rstd->p),
                  master(d, name + ".w"), dres ? dres->p : nullptr, grad(d, name + ".w"), grad(d, name + ".b"), T, h,
                  cs);
-    launches_ += wpk::layernorm_bwd(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p),
-                                    static_cast<float*>(st.rstd->p), master(d, name + ".w"),
-                                    dres ? dres->p : nullptr, dx->p, grad(d, name + ".w"), grad(d, name + ".b"), T, h,
-                                    cs);
+    timed_hbm(d, "layernorm_bwd", double(es) * T * h * (dres ? 4.0 : 3.0) + 8.0 * T + 20.0 * h, [&] {
+      launches_ += wpk::layernorm_bwd(dt, dln->p, st.x->p, static_cast<float*>(st.mean->p),
+                                      static_cast<float*>(st.rstd->p), master(d, name + ".w"),
+                                      dres ? dres->p : nullptr, dx->p, grad(d, name + ".w"), grad(d, name + ".b"), T,
+                                      h, cs);
+    });
     if (check_ops_enabled()) chk.after(dx->p, grad(d, name + ".w"), grad(d, name + ".b"), cs);
     return dx;
   };
@@ -892,7 +875,9 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
     // dU = (dY W2) * gelu'(U); the fc1 bias gradient (column sums of dU) in the same epilogue
     dgrad(dy->p, h, h, weight(d, L + "mlp.fc2.w"), f, du->p, wpk::kEpiDGelu, st.a->p, grad(d, L + "mlp.fc1.b"));
     wgrad(dy->p, h, st.b->p, f, grad(d, L + "mlp.fc2.w"));
-    if (!dy_bias_done) launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "mlp.fc2.b"), T, h, h, cs);
+    if (!dy_bias_done)
+      timed_hbm(d, "bias_colsum", double(es) * T * h + 8.0 * h,
+                [&] { launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "mlp.fc2.b"), T, h, h, cs); });
     wgrad(du->p, f, st.ln->p, h, grad(d, L + "mlp.fc1.w"));
     BufPtr dln = act(int64_t(T) * h);
     dgrad(du->p, f, f, weight(d, L + "mlp.fc1.w"), h, dln->p, wpk::kEpiStore, nullptr, nullptr, L + "ln2");
@@ -908,7 +893,9 @@ BufPtr Runtime::unit_bwd(DeviceState& d, int ui, int mb, UnitStash& st, BufPtr d
   dgrad(dy->p, h, h, weight(d, L + "attn.proj.w"), h, dctx->p, wpk::kEpiStore, nullptr, nullptr, std::string(),
         delta_fused);
   wgrad(dy->p, h, st.c->p, h, grad(d, L + "attn.proj.w"));
-  if (!dy_bias_done) launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "attn.proj.b"), T, h, h, cs);
+  if (!dy_bias_done)
+    timed_hbm(d, "bias_colsum", double(es) * T * h + 8.0 * h,
+              [&] { launches_ += wpk::colsum_accum(dt, dy->p, grad(d, L + "attn.proj.b"), T, h, h, cs); });
   BufPtr dqkv;
   if (use_flash()) {
     dqkv = act(int64_t(T) * 3 * h);
@@ -1037,7 +1024,36 @@ void Runtime::forward(DeviceState& d, const Action& a) {
   SliceStash& st = d.stash[{b, s}];
   st.units.assign(bounds_[s + 1] - bounds_[s], UnitStash{});
   for (int u = bounds_[s]; u < bounds_[s + 1]; ++u) x = unit_fwd(d, u, b, x, st.units[u - bounds_[s]]);
+  st.bytes = stash_bytes(st);
+  d.live_stash += st.bytes;
+  d.peak_stash = std::max(d.peak_stash, d.live_stash);
+  int64_t& sb = d.slice_stash_bytes[s];
+  sb = std::max(sb, st.bytes);
   if (s < list_.config.stages - 1) deliver(d, MsgKey{kAct, b, s}, x);
+}
+
+int64_t Runtime::stash_bytes(const SliceStash& st) {
+  std::vector<const Buf*> seen;
+  int64_t n = 0;
+  for (const UnitStash& u : st.units)
+    for (const BufPtr* b : {&u.x, &u.ln, &u.mean, &u.rstd, &u.a, &u.b, &u.c})
+      if (*b && std::find(seen.begin(), seen.end(), b->get()) == seen.end()) {
+        seen.push_back(b->get());
+        n += static_cast<int64_t>((*b)->bytes);
+      }
+  return n;
+}
+
+void Runtime::stash_stats(int pipe, int64_t* peak_bytes, int64_t* slice_bytes, int nslices) const {
+  if (pipe < 0 || pipe >= list_.config.devices || dev_of_pipeline_[pipe] < 0) {
+    throw wavepipe::ConfigError("stash_stats: pipeline device is not local to this process");
+  }
+  const DeviceState& d = *devs_[dev_of_pipeline_[pipe]];
+  *peak_bytes = d.peak_stash;
+  for (int s = 0; s < nslices; ++s) {
+    auto it = d.slice_stash_bytes.find(s);
+    slice_bytes[s] = it == d.slice_stash_bytes.end() ? 0 : it->second;
+  }
 }
 
 void Runtime::backward(DeviceState& d, const Action& a) {
@@ -1047,9 +1063,11 @@ void Runtime::backward(DeviceState& d, const Action& a) {
   if (it == d.stash.end()) throw wavepipe::SimulationError("runtime: backward before forward");
   SliceStash st = std::move(it->second);
   d.stash.erase(it);
+  const int64_t freed = st.bytes;
   d.bwd_unit_lo = bounds_[s];
   d.dy_bias_done = false;
   for (int u = bounds_[s + 1] - 1; u >= bounds_[s]; --u) dy = unit_bwd(d, u, b, st.units[u - bounds_[s]], dy);
+  d.live_stash -= freed;
   d.dy_bias_done = false;
   if (s > 0) deliver(d, MsgKey{kGrad, b, s - 1}, dy);
 }
@@ -1058,7 +1076,12 @@ void Runtime::optimizer(DeviceState& d) {
   if (grad_group_.size() > 1) dp_allreduce(d);
   if (!update_) return;
   wpk::OptimArgs o{m_.optimizer, m_.lr, m_.beta1, m_.beta2, m_.eps, m_.weight_decay, step_ + 1};
-  launches_ += wpk::optimizer_step(o, d.master, d.grad, d.m, d.v, d.shadow, d.nparam, d.compute);
+  // per parameter: master, grad (read, then zeroed), m, v read + written,
+  // the bf16 shadow written
+  const double per = (m_.optimizer == 1 ? 32.0 : 16.0) + (d.shadow ? 2.0 : 0.0);
+  timed_hbm(d, "optimizer", per * double(d.nparam), [&] {
+    launches_ += wpk::optimizer_step(o, d.master, d.grad, d.m, d.v, d.shadow, d.nparam, d.compute);
+  });
 }
 
 bool Runtime::advance(DeviceState& d) {
@@ -1073,6 +1096,7 @@ bool Runtime::advance(DeviceState& d) {
       if (!d.pending_ipc.empty()) ipc_land(d, a);
       d.last_start = next_event(d);
       ck(cudaEventRecord(d.last_start, d.compute), "record start");
+      d.starts.push_back({d.pc, d.last_start});
       if (a.kind == ActionKind::Forward) forward(d, a);
       else backward(d, a);
       if (tracing_) {
@@ -1090,40 +1114,6 @@ bool Runtime::advance(DeviceState& d) {
         if (a.kind == ActionKind::BatchedExchange) {
           const auto [q, qi] = d.be_partner[d.pc];
           ipc_post(d, message_key(list_.per_device[q][qi]));
-        }
-      }
-    } else if (transport_ == WP_TRANSPORT_NCCL) {
-      // Receives were posted at step start (post_channel_receives); here a
-      // Receive / the incoming half of an exchange only gates the next
-      // compute on that message's arrival.  Sends go out on the per-peer tx
-      // stream right after their producer -- buffered, never blocking compute.
-      auto arrive = [&](const MsgKey& kin) {
-        auto it = d.posted.find(kin);
-        if (it == d.posted.end()) throw wavepipe::SimulationError("runtime: message was not posted");
-        d.inbox[kin] = it->second.first;
-        d.pending.push_back(it->second.second);
-        d.posted.erase(it);
-      };
-      if (a.kind == ActionKind::Receive) {
-        arrive(message_key(a));
-      } else {
-        const MsgKey out = message_key(a);
-        auto it = d.outbox.find(out);
-        if (it == d.outbox.end()) throw wavepipe::SimulationError("runtime: send before its producer");
-        const Channel* ch = nullptr;
-        for (const Channel& c : channels_)
-          if (c.src == d.pipe && c.dst == a.peer) ch = &c;
-        cudaStream_t s = d.tx.at(a.peer);
-        ck(cudaStreamWaitEvent(s, d.outbox_ready[out], 0), "wait ready");
-        const size_t msg_bytes = size_t(m_.tokens()) * m_.hidden * m_.act_bytes();
-        ckn(NcclApi::get().Send(it->second->p, msg_bytes, ncclUint8, 1, static_cast<ncclComm_t>(ch->comm), s),
-            "ncclSend");
-        d.pool->release(it->second, s);
-        d.outbox.erase(it);
-        d.outbox_ready.erase(out);
-        if (a.kind == ActionKind::BatchedExchange) {
-          const auto [q, qi] = d.be_partner[d.pc];
-          arrive(message_key(list_.per_device[q][qi]));
         }
       }
     } else {
@@ -1181,19 +1171,41 @@ void Runtime::enqueue_step() {
   }
 }
 
-float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_device) {
+float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_device, cudaStream_t producer) {
+  if (broken_) throw wavepipe::SimulationError("runtime: a previous step stalled; create a new runtime");
   if (transport_ == WP_TRANSPORT_IPC && !ipc_connected_) {
     throw wavepipe::ConfigError("IPC transport: call ipc_connect with every rank's handle before the first step");
   }
   epoch_ = static_cast<uint32_t>(step_ + 1);
   for (auto& kv : ipc_send_next_) kv.second = 0;
   const size_t n = size_t(list_.config.microbatches) * m_.tokens();
+  if (on_device) {
+    // Device inputs: order the copies below after the producer's writes (the
+    // runtime's streams are non-blocking, so nothing else would).
+    cudaPointerAttributes attr{};
+    ck(cudaPointerGetAttributes(&attr, tokens), "token pointer attributes");
+    if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged) {
+      throw wavepipe::ConfigError("train_step: on_device set but tokens are not device memory");
+    }
+    DevGuard g(attr.device);
+    if (!input_ready_ || input_ready_dev_ != attr.device) {
+      if (input_ready_) {
+        DevGuard g0(input_ready_dev_);
+        cudaEventDestroy(input_ready_);
+      }
+      ck(cudaEventCreateWithFlags(&input_ready_, cudaEventDisableTiming), "event create");
+      input_ready_dev_ = attr.device;
+    }
+    ck(cudaEventRecord(input_ready_, producer), "record input ready");
+  }
   for (auto& d : devs_) {
     DevGuard g(d->cuda);
-    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    ck(cudaMemcpyAsync(d->tokens, tokens, n * sizeof(int32_t), on_device ? cudaMemcpyDefault : kind, d->compute),
+    if (on_device) ck(cudaStreamWaitEvent(d->compute, input_ready_, 0), "wait input producer");
+    ck(cudaMemcpyAsync(d->tokens, tokens, n * sizeof(int32_t), on_device ? cudaMemcpyDefault : cudaMemcpyHostToDevice,
+                       d->compute),
        "tokens H2D");
-    ck(cudaMemcpyAsync(d->labels, labels, n * sizeof(int32_t), on_device ? cudaMemcpyDefault : kind, d->compute),
+    ck(cudaMemcpyAsync(d->labels, labels, n * sizeof(int32_t), on_device ? cudaMemcpyDefault : cudaMemcpyHostToDevice,
+                       d->compute),
        "labels H2D");
     ck(cudaMemsetAsync(d->loss, 0, sizeof(float), d->compute), "loss reset");
     if (!update_) ck(cudaMemsetAsync(d->grad, 0, d->nparam * sizeof(float), d->compute), "grad reset");
@@ -1205,24 +1217,21 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     d->recs.clear();
     d->comm_recs.clear();
     d->gemm_recs.clear();
+    d->starts.clear();
     d->published_at.assign(list_.per_device[d->pipe].size(), 0);
     ck(cudaEventRecord(d->step_begin, d->compute), "record step begin");
     ck(cudaStreamWaitEvent(d->copy, d->step_begin, 0), "copy after begin");
-    if (transport_ == WP_TRANSPORT_NCCL) post_channel_receives(*d);
   }
   enqueue_step();
+  finish_step();
   float loss = 0.f;
   for (auto& d : devs_) {
     DevGuard g(d->cuda);
-    ck(cudaStreamSynchronize(d->copy), "step sync");
-    for (auto& kv : d->tx) ck(cudaStreamSynchronize(kv.second), "step sync");
-    for (auto& kv : d->rx) ck(cudaStreamSynchronize(kv.second), "step sync");
-    ck(cudaStreamSynchronize(d->compute), "step sync");
     float l = 0.f;
     ck(cudaMemcpy(&l, d->loss, sizeof(float), cudaMemcpyDeviceToHost), "loss D2H");
     loss += l;
     if (!d->stash.empty() || !d->handoff.empty() || !d->inbox.empty() || !d->outbox.empty() ||
-        !d->posted.empty() || !d->pending_ipc.empty() || !ipc_ready_.empty()) {
+        !d->pending_ipc.empty() || !ipc_ready_.empty()) {
       throw wavepipe::SimulationError("runtime: state left over at the end of the step");
     }
   }
@@ -1232,6 +1241,13 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     for (const auto& r : d->gemm_recs) {
       float ms = 0.f;
       ck(cudaEventElapsedTime(&ms, r.s, r.e), "gemm time");
+      if (r.hbm) {
+        auto& st = hbm_stats_[r.shape];
+        ++st.n;
+        st.flops += r.flops;
+        st.seconds += 1e-3 * ms;
+        continue;
+      }
       if (r.attention) {
         attn_seconds_ += 1e-3 * ms;
         attn_flops_ += r.flops;
@@ -1249,6 +1265,98 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
   }
   ++step_;
   return loss;
+}
+
+// Stall watchdog (ref src/simulate.cpp:160-165, SimulationError "simulation
+// stalled"; the executor contract's stall row, SURVEY.md 8a').  Every local
+// stream gets a completion event; the host polls them against the stall
+// timeout instead of blocking in cudaStreamSynchronize, so a dead, slow or
+// mismatched peer -- whose flags this rank's streams wait on -- surfaces as
+// an error naming the blocked action instead of a hang.
+void Runtime::finish_step() {
+  std::vector<std::pair<int, cudaEvent_t>> done;  // (cuda device, event)
+  for (auto& d : devs_) {
+    DevGuard g(d->cuda);
+    std::vector<cudaStream_t> streams{d->compute, d->copy};
+    if (d->sig) streams.push_back(d->sig);
+    for (auto& kv : d->tx) streams.push_back(kv.second);
+    for (cudaStream_t s : streams) {
+      cudaEvent_t e = next_event(*d);
+      ck(cudaEventRecord(e, s), "record stream done");
+      done.push_back({d->cuda, e});
+    }
+  }
+  static const bool dbg = std::getenv("WP_DEBUG_WATCHDOG") != nullptr;  // debugging aid
+  if (dbg) std::fprintf(stderr, "[wp] step %d enqueued; waiting on %zu streams\n", step_, done.size());
+  const auto t0 = std::chrono::steady_clock::now();
+  auto sleep_us = std::chrono::microseconds(0);
+  for (size_t i = 0; i < done.size();) {
+    DevGuard g(done[i].first);
+    const cudaError_t q = cudaEventQuery(done[i].second);
+    if (q == cudaSuccess) {
+      ++i;
+      continue;
+    }
+    if (q != cudaErrorNotReady) ck(q, "step");
+    const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (waited > stall_timeout_s_) stalled();
+    // Spin briefly, then back off to 1 ms polls (a step is >= milliseconds).
+    if (waited > 1e-3) sleep_us = std::min(std::chrono::microseconds(1000), sleep_us + std::chrono::microseconds(20));
+    if (sleep_us.count()) std::this_thread::sleep_for(sleep_us);
+  }
+}
+
+void Runtime::stalled() {
+  if (std::getenv("WP_DEBUG_WATCHDOG")) std::fprintf(stderr, "[wp] stall detected\n");
+  std::string where;
+  for (auto& d : devs_) {
+    DevGuard g(d->cuda);
+    const auto& prog = list_.per_device[d->pipe];
+    std::string what;
+    for (const auto& [pc, ev] : d->starts) {
+      if (cudaEventQuery(ev) == cudaErrorNotReady) {
+        what = "blocked at " + wavepipe::describe_action(prog[pc]) + " (position " + std::to_string(pc) +
+               "), waiting for its input";
+        break;
+      }
+    }
+    if (what.empty() && d->pc < prog.size()) what = "blocked at " + wavepipe::describe_action(prog[d->pc]);
+    if (what.empty()) {
+      what = cudaStreamQuery(d->compute) == cudaErrorNotReady
+                 ? "every compute started; blocked at the OptimizerStep (gradient all-reduce)"
+                 : "every compute done; a send is waiting for its receiver's post";
+    }
+    where += (where.empty() ? "" : "; ") + std::string("device ") + std::to_string(d->pipe) + " " + what;
+  }
+  cudaGetLastError();
+  broken_ = true;
+  // Release this rank's device-side waits: every wait of the step is on a
+  // flag of this rank's own arena (arrive / posted / all-reduce ready, done),
+  // so raising all of them to the epoch lets the streams drain and the
+  // runtime be freed.  The step's results are garbage; the runtime refuses
+  // further steps.
+  // Release this rank's device-side waits: every wait of the step is a
+  // bounded wait kernel (wpk::wait_flag) that also polls the host abort word,
+  // so one host store lets the streams drain and the runtime be freed.  The
+  // step's results are garbage; the runtime refuses further steps.
+  if (abort_host_) *abort_host_ = 1u;
+  const auto t0 = std::chrono::steady_clock::now();
+  while (!released_ && std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < 10.0) {
+    bool busy = false;
+    for (auto& d : devs_) {
+      DevGuard g(d->cuda);
+      for (cudaStream_t q : {d->compute, d->copy, d->sig})
+        if (q && cudaStreamQuery(q) == cudaErrorNotReady) busy = true;
+      for (auto& kv : d->tx)
+        if (cudaStreamQuery(kv.second) == cudaErrorNotReady) busy = true;
+    }
+    released_ = !busy;
+    if (busy) std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  }
+  cudaGetLastError();
+  if (std::getenv("WP_DEBUG_WATCHDOG")) std::fprintf(stderr, "[wp] device waits released: %d\n", int(released_));
+  throw wavepipe::SimulationError("runtime stalled (no progress for " + std::to_string(stall_timeout_s_) +
+                                  " s): " + where);
 }
 
 void Runtime::collect_trace() {

@@ -138,6 +138,14 @@ void Runtime::ipc_setup() {
   DevGuard g(d.cuda);
   StreamOps::get();  // fail at creation, not mid-step, if the driver lacks stream memory ops
   ck(cudaMalloc(&ipc_arena_, ipc_arena_bytes_), "cudaMalloc IPC arena");
+  // Abort word of the bounded waits: mapped pinned host memory the stall
+  // watchdog sets from the host (no stream needed to release a wait).
+  void* abort_mem = nullptr;
+  ck(cudaHostAlloc(&abort_mem, sizeof(uint32_t), cudaHostAllocMapped), "cudaHostAlloc abort word");
+  abort_host_ = static_cast<volatile uint32_t*>(abort_mem);
+  *abort_host_ = 0;
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&abort_dev_), const_cast<uint32_t*>(abort_host_), 0),
+     "abort word device pointer");
   ck(cudaMemset(ipc_arena_, 0, ipc_flag_bytes_), "memset IPC flags");
   ck(cudaDeviceSynchronize(), "IPC arena init");
   // One outgoing copy stream per peer this rank sends to; one signal stream.
@@ -239,6 +247,8 @@ void Runtime::ipc_release() {
   dp_grads_dev_ = nullptr;
   if (ipc_arena_) cudaFree(ipc_arena_);
   ipc_arena_ = nullptr;
+  if (abort_host_) cudaFreeHost(const_cast<uint32_t*>(abort_host_));
+  abort_host_ = nullptr;
   if (devs_[0]->sig) cudaStreamDestroy(devs_[0]->sig);
   devs_[0]->sig = nullptr;
 }
@@ -273,7 +283,7 @@ void Runtime::ipc_flush(DeviceState& d, int peer_dev) {
     if (it == ipc_ready_.end()) break;
     const IpcMsg& msg = ipc_msgs_[m];
     ck(cudaStreamWaitEvent(s, it->second.second, 0), "wait ready");
-    StreamOps::wait_geq(s, ipc_posted_flag(ipc_arena_, m), epoch_);
+    launches_ += wpk::wait_flag(s, ipc_posted_flag(ipc_arena_, m), epoch_, abort_dev_);
     cudaEvent_t t0 = nullptr;
     if (tracing_) {
       t0 = next_event(d);
@@ -316,7 +326,7 @@ void Runtime::ipc_land(DeviceState& d, const Action& a) {
     const auto [k, m] = d.pending_ipc[i];
     if (k.payload != want.payload || k.mb != want.mb || k.low != want.low) continue;
     const IpcMsg& msg = ipc_msgs_[m];
-    StreamOps::wait_geq(d.compute, ipc_arrive_flag(ipc_arena_, m), epoch_);
+    launches_ += wpk::wait_flag(d.compute, ipc_arrive_flag(ipc_arena_, m), epoch_, abort_dev_);
     BufPtr b = d.pool->alloc(message_bytes(), d.compute, 0);
     ck(cudaMemcpyAsync(b->p, ipc_arena_ + msg.data_off, message_bytes(), cudaMemcpyDeviceToDevice, d.compute),
        "IPC slot copy-out");
@@ -340,12 +350,12 @@ void Runtime::dp_allreduce(DeviceState& d) {
   for (int g = 0; g < G; ++g)
     if (g != group_me_) StreamOps::write(s, ipc_dp_flag(ipc_peer_[grad_group_[g]], 0, group_me_), epoch_);
   for (int g = 0; g < G; ++g)
-    if (g != group_me_) StreamOps::wait_geq(s, ipc_dp_flag(ipc_arena_, 0, g), epoch_);
+    if (g != group_me_) launches_ += wpk::wait_flag(s, ipc_dp_flag(ipc_arena_, 0, g), epoch_, abort_dev_);
   launches_ += wpk::allreduce_scaled_peers(dp_grads_dev_, G, group_me_, d.nparam, grad_scale_, s);
   for (int g = 0; g < G; ++g)
     if (g != group_me_) StreamOps::write(s, ipc_dp_flag(ipc_peer_[grad_group_[g]], 1, group_me_), epoch_);
   for (int g = 0; g < G; ++g)
-    if (g != group_me_) StreamOps::wait_geq(s, ipc_dp_flag(ipc_arena_, 1, g), epoch_);
+    if (g != group_me_) launches_ += wpk::wait_flag(s, ipc_dp_flag(ipc_arena_, 1, g), epoch_, abort_dev_);
 }
 
 }  // namespace wprt

@@ -55,6 +55,7 @@ class Pool {
   BufPtr alloc(size_t bytes, cudaStream_t stream, int pool_class);
   void release(const BufPtr& b, cudaStream_t stream);
   size_t reserved() const { return reserved_; }
+  void leak() { leak_ = true; }  // destructor skips cudaFree (streams blocked for good)
 
  private:
   int dev_;
@@ -62,6 +63,7 @@ class Pool {
   std::map<std::pair<int, size_t>, std::vector<BufPtr>> free_;
   std::vector<BufPtr> all_;
   size_t reserved_ = 0;
+  bool leak_ = false;
 };
 
 // Saved tensors of one unit for its backward.
@@ -71,6 +73,7 @@ struct UnitStash {
 
 struct SliceStash {
   std::vector<UnitStash> units;  // in unit order of the slice
+  int64_t bytes = 0;             // distinct stash buffers held (stash accounting)
 };
 
 struct MsgKey {
@@ -129,10 +132,13 @@ struct DeviceState;
 class Runtime {
  public:
   Runtime(const wp_model_desc& desc, const wavepipe::ActionList& list, int transport, const int* device_ids,
-          int rank, const void* nccl_id);
+          int rank);
   ~Runtime();
 
-  float train_step(const int32_t* tokens, const int32_t* labels, bool on_device);
+  // `producer`: the stream that wrote device-resident tokens/labels (nullptr:
+  // the legacy default stream of their device); the step waits for it.
+  float train_step(const int32_t* tokens, const int32_t* labels, bool on_device, cudaStream_t producer = nullptr);
+  void set_stall_timeout(double seconds) { stall_timeout_s_ = seconds; }
 
   const wavepipe::SimTrace& trace() const { return trace_; }
   void set_tracing(bool on) { tracing_ = on; }
@@ -155,6 +161,18 @@ class Runtime {
     prof_launches_ = 0, prof_flops_ = 0, prof_seconds_ = 0;
     attn_launches_ = 0, attn_flops_ = 0, attn_seconds_ = 0;
     prof_shapes_.clear();
+    hbm_stats_.clear();
+  }
+  // HBM-bound kernel classes timed while profiling: launches, algorithmic
+  // bytes, seconds.
+  int hbm_count() const { return static_cast<int>(hbm_stats_.size()); }
+  void hbm_stat(int i, const char** name, int64_t* n, double* bytes, double* seconds) const {
+    auto it = hbm_stats_.begin();
+    std::advance(it, i);
+    *name = it->first.c_str();
+    *n = it->second.n;
+    *bytes = it->second.flops;
+    *seconds = it->second.seconds;
   }
   // Per GEMM shape: "MxNxK b<batch> <A,B majorness> c<causal>" -> (launches, flops, seconds).
   std::string gemm_report() const;
@@ -163,6 +181,10 @@ class Runtime {
   // IPC landing slots (bytes).
   void memory(int64_t* pool_bytes, int64_t* landing_bytes) const;
 
+  // Stash of pipeline device `pipe` (local): peak live bytes, and per slice
+  // (index < nslices) the bytes of one (microbatch, slice) entry (0 if the
+  // slice is not on that device).
+  void stash_stats(int pipe, int64_t* peak_bytes, int64_t* slice_bytes, int nslices) const;
   int param_count() const { return static_cast<int>(param_index_.size()); }
   const ParamDesc& param_desc(int i, bool* owned) const;
   // IPC transport handshake: export this rank's landing arena (64-byte
@@ -192,6 +214,9 @@ class Runtime {
   void backward(DeviceState& d, const wavepipe::Action& a);
   void optimizer(DeviceState& d);
   void post_copy(DeviceState& dst, const MsgKey& key, Published msg);
+  static int64_t stash_bytes(const SliceStash& st);
+  void finish_step();          // watchdog-bounded wait for every local stream
+  [[noreturn]] void stalled(); // diagnose, release this rank's device waits, throw
   BufPtr take_input(DeviceState& d, const MsgKey& key);
   void deliver(DeviceState& d, const MsgKey& key, BufPtr buf);
   cudaEvent_t next_event(DeviceState& d);
@@ -225,26 +250,23 @@ class Runtime {
   // Profiling of one fused-attention launch (fwd or bwd) on the compute stream.
   template <typename F>
   void timed_attention(DeviceState& d, bool backward, F&& launch);
+  // Profiling of one HBM-bound kernel launch: class name, algorithmic bytes.
+  template <typename F>
+  void timed_hbm(DeviceState& d, const char* cls, double bytes, F&& launch);
   struct ShapeStat {
     int64_t n = 0;
     double flops = 0, seconds = 0;
   };
   std::map<std::string, ShapeStat> prof_shapes_;
+  std::map<std::string, ShapeStat> hbm_stats_;  // flops field = bytes
+  double stall_timeout_s_ = 300.0;
+  bool broken_ = false;    // a stalled step left the runtime unusable
+  bool released_ = false;  // ... and its device waits were released (safe to free)
+  cudaEvent_t input_ready_ = nullptr;
+  int input_ready_dev_ = -1;
   int step_ = 0;
   int64_t launches_ = 0;
   wavepipe::SimTrace trace_;
-  void* nccl_comm_ = nullptr;  // world communicator (NCCL transport)
-  // One communicator per directed device pair (sender rank 0, receiver rank
-  // 1 inside it) and the pair's messages in the sender's program order.
-  struct Channel {
-    int src, dst;
-    void* comm = nullptr;
-    std::vector<MsgKey> keys;
-  };
-  std::vector<Channel> channels_;
-  void build_channels();
-  void post_channel_receives(DeviceState& d);
-
   // CUDA-IPC transport (one process per GPU, copy-engine pushes over
   // NVLink); see ipc.cpp.  Every message m has a landing slot in its
   // receiver's arena (statically assigned from the receiver's program order,
@@ -269,6 +291,8 @@ class Runtime {
   std::map<MsgKey, int> ipc_index_;
   std::vector<IpcMsg> ipc_msgs_;
   char* ipc_arena_ = nullptr;
+  volatile uint32_t* abort_host_ = nullptr;  // stall release (mapped pinned host word)
+  uint32_t* abort_dev_ = nullptr;            // its device address
   size_t ipc_flag_bytes_ = 0, ipc_arena_bytes_ = 0;
   std::vector<char*> ipc_peer_;  // global rank -> mapped arena (nullptr: not a peer)
   bool ipc_connected_ = false, ipc_ok_ = false;

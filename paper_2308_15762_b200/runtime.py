@@ -14,7 +14,6 @@ from ._native import check, lib, wp_model_desc
 from .schedule import ActionList, SimTrace
 
 TRANSPORT_LOCAL = 0
-TRANSPORT_NCCL = 1
 TRANSPORT_IPC = 2
 IPC_HANDLE_BYTES = 128
 
@@ -58,13 +57,6 @@ class ModelDesc:
         return 3.0 * s * per_token
 
 
-def nccl_unique_id() -> bytes:
-    """128-byte ncclUniqueId (rank 0 creates it and broadcasts it)."""
-    buf = C.create_string_buffer(128)
-    check(lib.wp_nccl_unique_id(buf))
-    return buf.raw
-
-
 def _all_gather_bytes(blob: bytes):
     """Default IPC handshake: all-gather over the initialised torch.distributed
     group (rank order)."""
@@ -79,7 +71,6 @@ def _all_gather_bytes(blob: bytes):
 class Runtime:
     """wp_runtime_create / wp_train_step.  transport:
     TRANSPORT_LOCAL  all pipeline devices in this process (device_ids[d] per device);
-    TRANSPORT_NCCL   one process per pipeline device, NCCL send/recv (nccl_id);
     TRANSPORT_IPC    one process per GPU, copy-engine pushes into CUDA-IPC-mapped
                      landing slots; with schedule.config.replicas = D > 1 the job
                      has P*D ranks (rank = replica*P + pipeline device) and the
@@ -88,7 +79,7 @@ class Runtime:
                      the handles (default: torch.distributed)."""
 
     def __init__(self, model: ModelDesc, schedule: ActionList, transport=TRANSPORT_LOCAL, device_ids=None,
-                 rank=0, nccl_id=None, exchange=None):
+                 rank=0, exchange=None, stall_timeout=None):
         self.model = model
         self.schedule = schedule
         P = schedule.config.devices
@@ -96,14 +87,11 @@ class Runtime:
         ids = list(device_ids) if device_ids is not None else [0] * n_ids
         self._ids = (C.c_int * len(ids))(*ids)
         self._desc = model._c()
-        nid = None
-        if nccl_id is not None:
-            self._nccl = C.create_string_buffer(bytes(nccl_id), 128)
-            nid = C.cast(self._nccl, C.c_void_p)
         h = C.c_void_p()
-        check(lib.wp_runtime_create(C.byref(self._desc), schedule.handle, transport, self._ids, rank, nid,
-                                    C.byref(h)))
+        check(lib.wp_runtime_create(C.byref(self._desc), schedule.handle, transport, self._ids, rank, C.byref(h)))
         self._h = h
+        if stall_timeout is not None:
+            self.set_stall_timeout(stall_timeout)
         if transport == TRANSPORT_IPC:
             mine = C.create_string_buffer(IPC_HANDLE_BYTES)
             check(lib.wp_runtime_ipc_handle(self._h, mine))
@@ -113,6 +101,12 @@ class Runtime:
                 raise ValueError(f"exchange must return one {IPC_HANDLE_BYTES}-byte handle per rank")
             allh = C.create_string_buffer(b"".join(blobs), world * IPC_HANDLE_BYTES)
             check(lib.wp_runtime_ipc_connect(self._h, allh, world))
+
+    def set_stall_timeout(self, seconds):
+        """Watchdog: a step whose device work makes no progress for `seconds`
+        (a dead or mismatched peer) raises ScheduleError [1] naming the blocked
+        action; the runtime is unusable afterwards."""
+        check(lib.wp_runtime_set_stall_timeout(self._h, float(seconds)))
 
     def ipc_status(self):
         """(ok, message) of the IPC transport's set-up probe of its peers."""
@@ -133,17 +127,23 @@ class Runtime:
     def train_step(self, tokens, labels):
         """One synchronous step over all microbatches.  tokens/labels: int32
         [B, micro_batch_size, seq] as numpy arrays (host) or CUDA tensors
-        (device).  Returns the mean loss over microbatches."""
+        (device; the step waits for torch's current stream, which produced
+        them).  Returns the mean loss over microbatches."""
         on_dev = 0
+        stream = None
         if hasattr(tokens, "is_cuda"):
             on_dev = int(tokens.is_cuda)
+            if on_dev:
+                import torch
+                stream = torch.cuda.current_stream(tokens.device).cuda_stream
             tp, lp = tokens.data_ptr(), labels.data_ptr()
         else:
             tokens = np.ascontiguousarray(tokens, dtype=np.int32)
             labels = np.ascontiguousarray(labels, dtype=np.int32)
             tp, lp = tokens.ctypes.data, labels.ctypes.data
         loss = C.c_float()
-        check(lib.wp_train_step(self._h, C.c_void_p(tp), C.c_void_p(lp), on_dev, C.byref(loss)))
+        check(lib.wp_train_step_stream(self._h, C.c_void_p(tp), C.c_void_p(lp), on_dev, C.c_void_p(stream),
+                                       C.byref(loss)))
         return loss.value
 
     def set_tracing(self, on=True):
@@ -169,6 +169,15 @@ class Runtime:
         check(lib.wp_runtime_memory(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def stash(self, device):
+        """(peak live stash bytes, [bytes of one (microbatch, slice) entry per
+        slice]) of local pipeline device `device`."""
+        S = self.schedule.config.stages
+        peak = C.c_int64()
+        per = (C.c_int64 * S)()
+        check(lib.wp_runtime_stash(self._h, device, C.byref(peak), per, S))
+        return peak.value, list(per)
+
     def set_profiling(self, on=True):
         check(lib.wp_runtime_set_profiling(self._h, int(on)))
 
@@ -185,6 +194,18 @@ class Runtime:
         n, fl, sec = C.c_int64(), C.c_double(), C.c_double()
         check(lib.wp_runtime_attn_stats(self._h, C.byref(n), C.byref(fl), C.byref(sec)))
         return n.value, fl.value, sec.value
+
+    def hbm_stats(self):
+        """{kernel class: (launches, algorithmic bytes, summed seconds)} of the
+        HBM-bound kernels run while profiling was enabled."""
+        n = C.c_int()
+        check(lib.wp_runtime_hbm_count(self._h, C.byref(n)))
+        out = {}
+        for i in range(n.value):
+            name, k, b, sec = C.c_char_p(), C.c_int64(), C.c_double(), C.c_double()
+            check(lib.wp_runtime_hbm_stat(self._h, i, C.byref(name), C.byref(k), C.byref(b), C.byref(sec)))
+            out[name.value.decode()] = (k.value, b.value, sec.value)
+        return out
 
     def gemm_report(self):
         buf = C.create_string_buffer(1 << 16)

@@ -18,6 +18,7 @@ from ._native import (ConfigError, ScheduleError, check, lib, wp_action, wp_comm
                       wp_config, wp_cost, wp_interval)
 
 __all__ = [
+    "compare", "compare_measured",
     "Scheme", "ActionKind", "Payload", "Direction", "ScheduleConfig", "CostModel", "Action",
     "ActionList", "TraceInterval", "CommEvent", "SimTrace", "build_trace", "trace_to_gantt", "make_config", "generate_schedule",
     "insert_comm", "simulate", "bubble_ratio", "memory_profile", "activation_variance",
@@ -261,6 +262,43 @@ def trace_to_gantt(trace: SimTrace, fmt: str = "svg") -> str:
         return C.string_at(out).decode()
     finally:
         lib.wp_string_free(out)
+
+
+def _compare_text(fn_args, fmt):
+    out = C.c_void_p()
+    check(fn_args(0 if fmt == "csv" else 1, C.byref(out)))
+    try:
+        return C.string_at(out).decode()
+    finally:
+        lib.wp_string_free(out)
+
+
+def _requests(requests):
+    reqs = [(Scheme(r[0]), int(r[1])) if isinstance(r, tuple) else (Scheme(r), 1) for r in requests]
+    n = len(reqs)
+    return n, (C.c_int * max(n, 1))(*[int(s) for s, _ in reqs]), (C.c_int * max(n, 1))(*[w for _, w in reqs])
+
+
+def compare(requests, budget_devices, microbatches, cost: CostModel = None, fmt: str = "json") -> str:
+    """compare + compare_to_json / compare_to_csv (ref src/analytics.cpp:221-331):
+    requests are (Scheme, waves) pairs (or bare schemes, W=1) evaluated at one
+    device budget; returns the reference's CSV or JSON text, rows in
+    ascending makespan, failed rows last."""
+    n, sch, wav = _requests(requests)
+    k = (cost or CostModel())._c()
+    return _compare_text(lambda f, o: lib.wp_compare(sch, wav, n, budget_devices, microbatches, C.byref(k), f, o),
+                         fmt)
+
+
+def compare_measured(requests, budget_devices, microbatches, traces, lists, fmt: str = "json") -> str:
+    """The same rows from measured traces (one per request, e.g. the GPU
+    runtime's train_step traces of lists[i]): makespan in seconds, the
+    bubble ratio of the measured trace."""
+    n, sch, wav = _requests(requests)
+    tr = (C.c_void_p * max(n, 1))(*[t._h for t in traces])
+    ls = (C.c_void_p * max(n, 1))(*[x.handle for x in lists])
+    return _compare_text(lambda f, o: lib.wp_compare_measured(sch, wav, n, budget_devices, microbatches, tr, ls, f,
+                                                              o), fmt)
 
 
 def simulate(lst: ActionList, cost: CostModel = None) -> SimTrace:

@@ -33,3 +33,69 @@ def test_gpu_arm_fails_loudly_without_gpu():
                           "--model", "tiny-gpt", "--no-cpu-baseline"], capture_output=True, text=True, timeout=600,
                          cwd=ROOT)
     assert out.returncode != 0
+
+
+def test_reference_arm_never_loads_the_product():
+    """The reference arm runs only oracle/ code: the product package is never
+    imported and libwavepipe.so is never mapped into its process."""
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0', "
+            "'--model', 'tiny-gpt']; runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('LOADED', 'libwavepipe' in maps, any(m.startswith('paper_2308_15762_b200') for m in sys.modules))")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == "LOADED False False"
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """Launched like the driver's N=2 reference arm: rank 0 alone prints one
+    line, describing P=2 (config and schedule timing agree)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port=29533", os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+           "--steps", "1", "--warmup", "0", "--model", "tiny-gpt"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "pp2"
+    assert "P=2" in line["config"]["schedule"]
+
+
+def test_spawn_command_for_n_gpus():
+    """`bench.py --gpus N` outside torchrun re-launches itself as N ranks."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    cmd = bench.spawn_command(8, ["--gpus", "8", "--steps", "3"])
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=8" in cmd and "127.0.0.1" in cmd
+    assert cmd[-4:] == [os.path.join(ROOT, "bench.py"), "--gpus", "8", "--steps", "3"][-4:]
+
+
+def test_gpu_arm_rejects_mismatched_world_size():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--model", "tiny-gpt"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE" in (out.stderr + out.stdout)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+def test_gpu_arm_spawns_its_ranks():
+    """`python bench.py --gpus 2` without torchrun runs two ranks (here both on
+    the box's one GPU, WP_BENCH_SHARE_GPU=1: functional, not a measurement)
+    and rank 0 prints one line with n_gpus 2 over the IPC transport."""
+    env = dict(os.environ, WP_BENCH_SHARE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup",
+                          "1", "--model", "tiny-gpt", "--mbs", "2", "--no-cpu-baseline"], capture_output=True,
+                         text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "pp2"
+    assert line["p2p"]["transport"] == "ipc" and line["p2p"]["messages"] > 0
+    assert line["gpu_launches"] > 0 and line["hbm"]["kernels"]

@@ -134,6 +134,24 @@ def test_tc_pair_split_k_accumulation(shape):
     torch.testing.assert_close(out, ref, rtol=1e-3, atol=2e-3 * K ** 0.5)
 
 
+@pytest.mark.parametrize("which", ["logits", "dgrad", "wgrad"])
+def test_lm_head_vocab_50304(which):
+    """The GPT-1.3B LM head at its own shapes (V = 50304 = 196.5 x 256: a
+    ragged last N tile for the logits, a ragged last K block for the data
+    gradient, a ragged last M tile for the fp32 weight gradient); T = 2048
+    tokens, h = 2048."""
+    T, h, V = 2048, 2048, 50304
+    if which == "logits":   # logits[T, V] = LN[T, h] @ wte[V, h]^T, bf16 store
+        out, ref = run(T, V, h, False, False, torch.bfloat16)
+        torch.testing.assert_close(out, ref, rtol=2e-2, atol=2e-2 * 8)
+    elif which == "dgrad":  # dLN[T, h] = dlogits[T, V] @ wte[V, h]
+        out, ref = run(T, h, V, False, True, torch.bfloat16, c_dtype=torch.float32)
+        torch.testing.assert_close(out, ref, rtol=1e-3, atol=2e-3 * V ** 0.5)
+    else:                   # dwte[V, h] += dlogits^T @ LN  (both MN-major over T)
+        out, ref = run(V, h, T, True, True, torch.bfloat16, mode=EPI_ACCUM, c_dtype=torch.float32)
+        torch.testing.assert_close(out, ref, rtol=1e-3, atol=2e-3 * T ** 0.5)
+
+
 lib.wp_debug_gemm_colsum.restype = C.c_int
 lib.wp_debug_gemm_colsum.argtypes = [C.c_int] * 4 + [C.c_void_p, C.c_int64, C.c_int] * 2 + \
     [C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]

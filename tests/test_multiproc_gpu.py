@@ -85,6 +85,7 @@ def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q, D=1, sc
         msg = desc.micro_batch_size * desc.seq * desc.hidden * (4 if dtype == "fp32" else 2)
         _, landing = rt.memory()
         assert landing <= 2 * ((msg + 255) // 256 * 256), (landing, msg)
+        _check_stash(wp, rt, sched, rank % P)
         all_losses = [None] * world
         dist.all_gather_object(all_losses, losses)
         rt.close()
@@ -94,6 +95,102 @@ def _worker(rank, world, port, B, W, dtype, optimizer, steps, update, q, D=1, sc
         q.put((rank, repr(e), None))
     finally:
         dist.destroy_process_group()
+
+
+def _check_stash(wp, rt, sched, pipe):
+    """This rank's activation stash follows the reference's liveness and
+    stays within memory_profile's peak units x bytes per unit (ref
+    src/analytics.cpp:48-91; a slice's unit fraction from the placement)."""
+    from fractions import Fraction
+    peak, per_slice = rt.stash(pipe)
+    live = best = 0
+    for a in sched.per_device[pipe]:
+        if a.kind == wp.ActionKind.Forward:
+            live += per_slice[a.slice_index]
+            best = max(best, live)
+        elif a.kind == wp.ActionKind.Backward:
+            live -= per_slice[a.slice_index]
+    assert peak == best, (pipe, peak, best)
+    cfg = sched.config
+    if not any(per_slice):  # every slice of this device is empty (S > units)
+        assert peak == 0
+        return
+    if cfg.scheme == wp.Scheme.Hanayo:
+        _, peaks = wp.memory_profile(wp.simulate(sched, wp.CostModel(1.0, 2.0, 0.0)), sched)
+        unit = max(Fraction(b) * 2 * cfg.waves for b in per_slice if b)
+        assert peak <= peaks[pipe] * unit, (pipe, peak, float(peaks[pipe] * unit))
+
+
+def _stall_worker(rank, world, port, q):
+    """Rank 1 connects but never steps: rank 0's step must fail with the
+    stall error naming its blocked action, then free cleanly."""
+    import faulthandler
+    import sys
+    import torch.distributed as dist
+    faulthandler.dump_traceback_later(150, exit=True, file=sys.stderr)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import time
+        import paper_2308_15762_b200 as wp
+        from paper_2308_15762_b200.data import synthetic_batch
+        torch.cuda.set_device(0)
+        desc = _desc("fp32")
+        sched = wp.generate_schedule(wp.make_config(wp.Scheme.Hanayo, 2, 4, 2))
+        rt = wp.Runtime(desc, sched, transport=wp.TRANSPORT_IPC, device_ids=[0], rank=rank, stall_timeout=3.0)
+        result = "idle"
+        if rank == 0:
+            tokens, labels = synthetic_batch(4, desc.micro_batch_size, desc.seq, desc.vocab)
+            t0 = time.time()
+            try:
+                rt.train_step(tokens, labels)
+                result = "no error"
+            except wp.ScheduleError as e:
+                result = (e.code, str(e), time.time() - t0)
+            try:
+                rt.train_step(tokens, labels)
+                result = "second step ran"
+            except wp.ScheduleError:
+                pass
+            rt.close()  # must not hang: the stalled waits were released
+        dist.barrier()
+        if rank == 1:
+            rt.close()
+        q.put((rank, result))
+    except Exception as e:
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_stall_watchdog_names_blocked_action():
+    """Executor contract, stall row (ref src/simulate.cpp:160-165): a peer that
+    never runs its program makes the step return error code 1 (semantic,
+    the reference's SimulationError) within the stall timeout, naming the
+    action this rank is blocked at -- not a hang."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stall_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    try:
+        for _ in range(2):
+            r, res = q.get(timeout=200)
+            out[r] = res
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    assert isinstance(out[0], tuple), out
+    code, msg, waited = out[0]
+    assert code == 1, out[0]
+    assert "stalled" in msg and "blocked at" in msg and "device 0" in msg, msg
+    assert 2.5 <= waited < 60, waited
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
 
 
 def _spawn(world, B, W, dtype, optimizer="sgd", steps=1, update=False, D=1):

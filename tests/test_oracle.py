@@ -10,6 +10,7 @@ import json
 import math
 import os
 
+import numpy as np
 import pytest
 import torch
 
@@ -104,3 +105,16 @@ def test_model_oracle_initial_loss_and_fd_gradients():
             t.view(-1)[i] = orig
             fd = (fp - fm) / (2 * eps)
             assert abs(fd - grads[name].view(-1)[i].item()) <= 1e-6 + 1e-5 * abs(fd)
+
+
+def test_oracle_input_stream_matches_product():
+    """oracle/data.py restates the SURVEY 8(d) input spec; it must produce the
+    product's batches bit for bit (causal and bidirectional, several steps)."""
+    from oracle import data as od
+    from paper_2308_15762_b200 import data as pd
+    for causal in (True, False):
+        for step in (0, 3):
+            a = od.synthetic_batch(3, 2, 64, 50304, causal=causal, step=step)
+            b = pd.synthetic_batch(3, 2, 64, 50304, causal=causal, step=step)
+            for x, y in zip(a, b):
+                assert x.dtype == y.dtype and x.shape == y.shape and np.array_equal(x, y)
