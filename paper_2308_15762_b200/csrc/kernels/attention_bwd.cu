@@ -21,6 +21,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -56,7 +57,7 @@ struct BwCfg {
   static constexpr int PT = T128 * T128 * 2;    // dS^T tile
   static constexpr int STAGE = 4 * 2 * SLAB_BYTES;  // dQ drain: 2 fp32 slabs per drain warp
   // K, V, Q[2], dO, dS^T, drain slabs, lse/delta (single-buffered), barriers
-  static constexpr int SMEM = 5 * TILE + PT + STAGE + 2 * T128 * 4 + 1024 + 256;
+  static constexpr int SMEM = 5 * TILE + PT + STAGE + 2 * T128 * 4 + 1024 + 256;  // 16 barriers + TMEM slot
   static constexpr uint32_t kColDK = kColDV + D;
 };
 
@@ -84,6 +85,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
 
 struct BwParams {
   int batch, seq, heads, n_tiles, causal, hidden;
+  int group;  // (batch, head) pairs per raster group (0: all)
   float scale_log2, scale;
   const float* lse2;
   const float* delta;
@@ -135,15 +137,24 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   uint64_t* dp_full = bars + 11;
   uint64_t* do_full = bars + 12;
   uint64_t* do_empty = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* p_full = bars + 14;  // P^T of the tile written to TMEM (dV may start)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // Heaviest-first (LPT) order: all (batch, head) CTAs of key tile 0 -- the
-  // most causal query tiles -- launch before those of tile 1, and so on.
-  const int bh = p.batch * p.heads;
-  const int kj = static_cast<int>(blockIdx.x / bh);
-  const int head = static_cast<int>(blockIdx.x % bh % p.heads);
-  const int b = static_cast<int>(blockIdx.x % bh / p.heads);
+  // Raster: groups of p.group (batch, head) pairs; inside a group,
+  // heaviest-first (LPT): every pair's key tile 0 -- the most causal query
+  // tiles -- before tile 1, and so on.  A group's fp32 dQ accumulator
+  // (p.group x seq x D x 4 bytes) and its Q / dO stay L2-resident while all
+  // its key tiles reduce into / read them.
+  const int bh_all = p.batch * p.heads;
+  const int G = p.group > 0 && p.group < bh_all ? p.group : bh_all;
+  const int grp = static_cast<int>(blockIdx.x / (p.n_tiles * G));
+  const int gsz = min(G, bh_all - grp * G);
+  const int rem = static_cast<int>(blockIdx.x - grp * p.n_tiles * G);
+  const int kj = rem / gsz;
+  const int bhi = grp * G + rem % gsz;
+  const int head = bhi % p.heads;
+  const int b = bhi / p.heads;
   const int i0 = p.causal ? kj : 0;
   const int n_it = p.n_tiles - i0;
 
@@ -166,6 +177,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     mbar_init(dq_free, 4);
     mbar_init(dkv_done, 1);
     mbar_init(dp_full, 1);
+    mbar_init(p_full, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -243,22 +255,30 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         }
         tc_commit(dp_full);
       };
-      issue_s(0);
-      issue_dp(0);
-      for (int it = 0; it < n_it; ++it) {
-        const int x = it & 1;
-        const uint64_t dQm = make_desc(smem_u32(sQ + x * Cfg::TILE), ATOM, 1024);
-        mbar_wait(ds_full, it & 1);
+      // dV(it) += P^T(it) dO(it), P^T from TMEM (queries [0,64) at columns
+      // 0.., [64,128) at 64..), as soon as the softmax warps wrote P^T --
+      // before dS^T(it) exists, so S^T(it+1) can follow right away and the
+      // next tile's P^T overlaps this tile's dS^T.
+      auto issue_dv = [&](int it) {
+        mbar_wait(p_full, it & 1);
         tc_fence_after();
-        BWT(1, it);
-        // dV += P^T dO (P^T from TMEM: queries [0,64) at columns 0.., [64,128) at 64..)
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k)
           tc_mma_ts(tmem + kColDV, tmem + kColS + (k >> 2) * 64 + (k & 3) * 8, desc_add(dDOm, k * 2048), id_kv,
                     (it | k) != 0);
         tc_commit(do_empty);
+      };
+      issue_s(0);
+      issue_dp(0);
+      issue_dv(0);
+      for (int it = 0; it < n_it; ++it) {
+        const int x = it & 1;
+        const uint64_t dQm = make_desc(smem_u32(sQ + x * Cfg::TILE), ATOM, 1024);
         // S^T(it+1) over the P^T(it) columns: in order after dV(it), which read them
         if (it + 1 < n_it) issue_s(it + 1);
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+        BWT(1, it);
         BWT(3, it);
         // dK += dS^T Q (reduction over the 128 queries)
 #pragma unroll
@@ -275,7 +295,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         tc_commit(dq_full);
         tc_commit(pds_free);
         BWT(2, it);
-        if (it + 1 < n_it) issue_dp(it + 1);  // after the drain read dQ(it) out of TMEM
+        if (it + 1 < n_it) {
+          issue_dp(it + 1);  // after the drain read dQ(it) out of TMEM
+          issue_dv(it + 1);
+        }
       }
       tc_commit(dkv_done);
     }
@@ -323,6 +346,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) pv[h2 * 32 + i] *= p.scale;  // dS = (dP - Delta) * (P / sqrt(D))
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);  // P^T in TMEM: dV(it) may start
       if (warp == 4 && lane == 0) BWT(6, it);
       // Phase B: dS^T = P^T * (dP^T - Delta) / sqrt(D) once dP^T is in.
       mbar_wait(dp_full, it & 1);
@@ -572,6 +599,11 @@ void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const flo
   p.dq_acc = dq_acc;
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   p.dbias = dbias;
+  static const int group = [] {
+    const char* g = std::getenv("WP_BW_GROUP");  // A/B switch; 0 = one group
+    return g ? std::atoi(g) : 0;
+  }();
+  p.group = group;
   const int grid = p.n_tiles * s.heads * s.mbs;
   const CUtensorMap mdq = make_slab_map(dq_acc, kF32, s.hidden, int64_t(s.mbs) * s.seq, s.hidden);
   k<<<grid, BW_THREADS, BwCfg<D>::SMEM, stream>>>(mq, mk, mv, mdo, mdq, p);
