@@ -12,7 +12,7 @@ LIB      := $(PKG)/libwavepipe.so
 INCLUDES := -Iinclude -I$(CSRC) -I$(CUDA)/include
 CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra $(INCLUDES)
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
+NVFLAGS  := $(EXTRA_NVFLAGS) -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
             --expt-relaxed-constexpr -Xptxas -v $(INCLUDES)
 
 CORE_SRCS := $(wildcard $(CSRC)/core/*.cpp) $(wildcard $(CSRC)/*.cpp) $(wildcard $(CSRC)/runtime/*.cpp)

@@ -1,26 +1,31 @@
 // Flash attention backward on the 5th-gen tensor cores (sm_100a).
 //
-// One CTA per (128-key tile j, head, sequence); K_j and V_j stay in shared
+// Work item = (128-key tile j, head, sequence): K_j and V_j stay in shared
 // memory while the query tiles i (causal: i >= j) stream through.  Per q tile:
 //   MMA        S^T  = K_j Q_i^T      (M=keys, N=queries, K=D)   -> TMEM
 //              dP^T = V_j dO_i^T     (M=keys, N=queries, K=D)   -> TMEM
-//   softmax    4 warps, one key row per thread:  P^T = 2^(t - lse2),
+//   softmax    8 warps, one key row per thread, two query halves:
+//              P^T = 2^(s - lse2) -> bf16 back into TMEM (A of dV);
 //              dS^T = P^T * (dP^T - Delta) / sqrt(D)  -> bf16 -> smem (SW128)
-//   MMA        dV_j += P^T dO_i,  dK_j += dS^T Q_i        (TMEM accumulators)
-//              dQ_i  = dS K_j     (A = the dS^T tile read MN-major)
+//   MMA        dV_j += P^T dO_i (A from TMEM), dK_j += dS^T Q_i (accumulators
+//              in TMEM), dQ_i = dS K_j (A = the dS^T tile read MN-major)
 //   dQ warps   4 warps drain dQ_i from TMEM through their own fp32 SW128
 //              slabs with TMA bulk reduce-adds into an fp32 accumulator
-//              (every key tile contributes to each q tile)
-// Issue order per q tile: dV_j(i), S^T(i+1) (into the P^T columns dV just
-// read), dK_j(i), dQ_i, then dP^T(i+1) once dQ_i is out of TMEM -- so the
-// softmax of tile i+1 overlaps dK/dQ of tile i and the dQ drain, whose L2
-// reduce-adds no longer hold the dS^T buffer.
-// Delta = rowsum(dO * O) comes from attn_bwd_prep; dq_finish converts the fp32
-// dQ accumulator to bf16 into dqkv.  dK, dV are written at the end.
+//              (every key tile contributes to each q tile); after an item's
+//              last tile they also write its dK / dV rows
+// Issue order (FA4's): S^T(i+1), dQ_i (two D halves, own commits), dK_j(i),
+// dP^T(i+1) once the drain read dQ_i out of the shared columns, dV(i+1) as
+// soon as P^T(i+1) is in TMEM -- the next tile's softmax overlaps this
+// tile's dQ / dK and the drain.  Persistent CTAs (one per SM) walk the items
+// in a grouped, heaviest-first raster (see bw_item); lse / Delta of each
+// tile arrive by bulk copy off the softmax critical path.
+// Delta = rowsum(dO * O) comes from the projection GEMM's epilogue (or
+// attn_bwd_prep); dq_finish converts the fp32 dQ accumulator to bf16 into dqkv.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -31,11 +36,11 @@
 namespace wpk {
 #ifdef WP_BW_TRACE
 // Debug timeline of CTA 0 (build with -DWP_BW_TRACE; tools/bw_trace_probe.py):
-// clock64 per (event, q tile).
+// clock64 per (event, global tile g < 32).
 __device__ unsigned long long g_bwt[16 * 32];
-#define BWT(ev, j)                                                                    \
-  do {                                                                                \
-    if (blockIdx.x == 0 && (j) < 32) g_bwt[(ev) * 32 + (j)] = clock64();             \
+#define BWT(ev, j)                                                        \
+  do {                                                                    \
+    if (blockIdx.x == 0 && (j) < 32) g_bwt[(ev) * 32 + (j)] = clock64(); \
   } while (0)
 #else
 #define BWT(ev, j) \
@@ -105,9 +110,37 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {  // 16-B chunk c of row 
   return atom * ATOM + (r >> 3) * 1024 + (r & 7) * 128 + ((cc ^ (r & 7)) << 4);
 }
 
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 
+// One work item = (key tile kj, batch b, head).  Items in raster order:
+// groups of p.group (batch, head) pairs; inside a group heaviest-first (LPT):
+// every pair's key tile 0 -- the most causal query tiles -- before tile 1,
+// and so on.  A group's fp32 dQ accumulator and its Q / dO stay L2-resident
+// while all its key tiles reduce into / read them.
+struct BwItem {
+  int kj, b, head, i0, n_it;
+};
+__device__ __forceinline__ BwItem bw_item(const BwParams& p, int w) {
+  const int bh_all = p.batch * p.heads;
+  const int G = p.group > 0 && p.group < bh_all ? p.group : bh_all;
+  const int grp = w / (p.n_tiles * G);
+  const int gsz = min(G, bh_all - grp * G);
+  const int rem = w - grp * p.n_tiles * G;
+  BwItem it;
+  it.kj = rem / gsz;
+  const int bhi = grp * G + rem % gsz;
+  it.head = bhi % p.heads;
+  it.b = bhi / p.heads;
+  it.i0 = p.causal ? it.kj : 0;
+  it.n_it = p.n_tiles - it.i0;
+  return it;
+}
+
+// Persistent: one CTA per SM walks items w = blockIdx.x, + gridDim.x, ...
+// Per-tile barriers run on the CTA's global tile counter g (across items),
+// per-item ones on its item counter, so the next item's K/V load, S^T and
+// dP^T overlap the previous item's dK / dV epilogue (done by the dQ drain
+// warps), and TMEM / barriers are set up once.
 template <int D>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     flash_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
@@ -123,7 +156,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   uint8_t* sDS = sDO + Cfg::TILE;     // dS^T [keys x queries]
   uint8_t* sStage = sDS + Cfg::PT;    // dQ drain slabs
   float* sLse = reinterpret_cast<float*>(sStage + Cfg::STAGE);  // [128]
-  float* sDelta = sLse + T128;                            // [128]
+  float* sDelta = sLse + T128;                                   // [128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sDelta + T128);
   uint64_t* kv_full = bars + 0;
   uint64_t* q_full = bars + 1;   // [2]
@@ -137,26 +170,18 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   uint64_t* dp_full = bars + 11;
   uint64_t* do_full = bars + 12;
   uint64_t* do_empty = bars + 13;
-  uint64_t* p_full = bars + 14;  // P^T of the tile written to TMEM (dV may start)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* p_full = bars + 14;    // P^T of the tile written to TMEM (dV may start)
+  uint64_t* lse_full = bars + 15;  // the tile's lse / Delta rows landed (bulk copies by warp 3)
+  uint64_t* dl_full = bars + 16;
+  uint64_t* kv_empty = bars + 17;  // the item's last MMA read K / V
+  uint64_t* dkv_free = bars + 18;  // the item's dK / dV read out of TMEM (epilogue)
+  // The drain reads dQ in two D halves, each with its full / free barrier.
+  uint64_t* dq_full_h[2] = {dq_full, bars + 19};
+  uint64_t* dq_free_h[2] = {dq_free, bars + 20};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // Raster: groups of p.group (batch, head) pairs; inside a group,
-  // heaviest-first (LPT): every pair's key tile 0 -- the most causal query
-  // tiles -- before tile 1, and so on.  A group's fp32 dQ accumulator
-  // (p.group x seq x D x 4 bytes) and its Q / dO stay L2-resident while all
-  // its key tiles reduce into / read them.
-  const int bh_all = p.batch * p.heads;
-  const int G = p.group > 0 && p.group < bh_all ? p.group : bh_all;
-  const int grp = static_cast<int>(blockIdx.x / (p.n_tiles * G));
-  const int gsz = min(G, bh_all - grp * G);
-  const int rem = static_cast<int>(blockIdx.x - grp * p.n_tiles * G);
-  const int kj = rem / gsz;
-  const int bhi = grp * G + rem % gsz;
-  const int head = bhi % p.heads;
-  const int b = bhi / p.heads;
-  const int i0 = p.causal ? kj : 0;
-  const int n_it = p.n_tiles - i0;
+  const int n_items = p.n_tiles * p.batch * p.heads;
 
   if (warp == 0 && lane == 0) {
     for (const CUtensorMap* m : {&map_q, &map_k, &map_v, &map_do})
@@ -164,6 +189,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   }
   if (warp == 1 && lane == 0) {
     mbar_init(kv_full, 1);
+    mbar_init(kv_empty, 1);
     for (int x = 0; x < 2; ++x) {
       mbar_init(&q_full[x], 1);
       mbar_init(&q_empty[x], 1);
@@ -173,11 +199,16 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     mbar_init(s_full, 1);
     mbar_init(ds_full, 8);
     mbar_init(pds_free, 1);  // dK and dQ MMAs done reading dS^T
-    mbar_init(dq_full, 1);
-    mbar_init(dq_free, 4);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(dq_full_h[h], 1);
+      mbar_init(dq_free_h[h], 4);
+    }
     mbar_init(dkv_done, 1);
+    mbar_init(dkv_free, 4);
     mbar_init(dp_full, 1);
     mbar_init(p_full, 8);
+    mbar_init(lse_full, 1);
+    mbar_init(dl_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -192,24 +223,52 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(kv_full, 2 * Cfg::TILE);
+      int g = 0;  // global tile counter
+      int ip = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ip) {
+        const BwItem itm = bw_item(p, w);
+        for (int t = 0; t < itm.n_it; ++t, ++g) {  // Q double-buffered (two tiles ahead), dO single
+          const int qi = itm.i0 + t, x = g & 1;
+          if (g >= 2) mbar_wait(&q_empty[x], ((g - 2) >> 1) & 1);
+          mbar_expect_tx(&q_full[x], Cfg::TILE);
 #pragma unroll
-      for (int a = 0; a < D / 64; ++a) {
-        tma_load_4d(&map_k, kv_full, sK + a * ATOM, a * 64, head, kj * T128, b);
-        tma_load_4d(&map_v, kv_full, sV + a * ATOM, a * 64, head, kj * T128, b);
+          for (int a = 0; a < D / 64; ++a)
+            tma_load_4d(&map_q, &q_full[x], sQ + x * Cfg::TILE + a * ATOM, a * 64, itm.head, qi * T128, itm.b);
+          if (g >= 1) mbar_wait(do_empty, (g - 1) & 1);  // dV(g-1) read dO(g-1)
+          mbar_expect_tx(do_full, Cfg::TILE);
+#pragma unroll
+          for (int a = 0; a < D / 64; ++a)
+            tma_load_4d(&map_do, do_full, sDO + a * ATOM, a * 64, itm.head, qi * T128, itm.b);
+          if (t == 0) {  // K / V after the first Q / dO: those buffers free up earlier
+            if (ip > 0) mbar_wait(kv_empty, (ip - 1) & 1);  // previous item's MMAs done with K / V
+            mbar_expect_tx(kv_full, 2 * Cfg::TILE);
+#pragma unroll
+            for (int a = 0; a < D / 64; ++a) {
+              tma_load_4d(&map_k, kv_full, sK + a * ATOM, a * 64, itm.head, itm.kj * T128, itm.b);
+              tma_load_4d(&map_v, kv_full, sV + a * ATOM, a * 64, itm.head, itm.kj * T128, itm.b);
+            }
+          }
+        }
       }
-      for (int it = 0; it < n_it; ++it) {  // Q double-buffered (two tiles ahead), dO single
-        const int qi = i0 + it, x = it & 1;
-        if (it >= 2) mbar_wait(&q_empty[x], ((it - 2) >> 1) & 1);
-        mbar_expect_tx(&q_full[x], Cfg::TILE);
-#pragma unroll
-        for (int a = 0; a < D / 64; ++a)
-          tma_load_4d(&map_q, &q_full[x], sQ + x * Cfg::TILE + a * ATOM, a * 64, head, qi * T128, b);
-        if (it >= 1) mbar_wait(do_empty, (it - 1) & 1);  // dV(it-1) read dO(it-1)
-        mbar_expect_tx(do_full, Cfg::TILE);
-#pragma unroll
-        for (int a = 0; a < D / 64; ++a)
-          tma_load_4d(&map_do, do_full, sDO + a * ATOM, a * 64, head, qi * T128, b);
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // lse and Delta of each query tile, single-buffered: the tile's lse
+      // as soon as the softmax warps finished phase A of the previous tile
+      // (p_full), its Delta once they finished phase B (ds_full) -- each
+      // lands while the other phase runs, off the softmax critical path.
+      int g = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+        const BwItem itm = bw_item(p, w);
+        for (int t = 0; t < itm.n_it; ++t, ++g) {
+          const int64_t vec = (static_cast<int64_t>(itm.b) * p.heads + itm.head) * p.seq + (itm.i0 + t) * T128;
+          if (g > 0) mbar_wait(p_full, (g - 1) & 1);
+          mbar_expect_tx(lse_full, T128 * 4);
+          bulk_load(sLse, p.lse2 + vec, T128 * 4, lse_full);
+          if (g > 0) mbar_wait(ds_full, (g - 1) & 1);
+          mbar_expect_tx(dl_full, T128 * 4);
+          bulk_load(sDelta, p.delta + vec, T128 * 4, dl_full);
+        }
       }
     }
   } else if (warp == 1) {
@@ -221,18 +280,19 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       constexpr uint32_t id_kv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) |
                                  (uint32_t(T128 >> 4) << 24);
       constexpr uint32_t id_dq = id_kv | (1u << 15);
+      constexpr uint32_t id_dq_half = (id_dq & ~(0x3Fu << 17)) | (uint32_t(64 >> 3) << 17);  // N=64 (D=128 halves)
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aDS = smem_u32(sDS);
       // K-major (k-step offsets in-atom) and MN-major (2 KB per 16 rows) descriptors
       const uint64_t dK = make_desc(aK, 16, 1024), dV = make_desc(aV, 16, 1024), dDS = make_desc(aDS, 16, 1024);
       const uint64_t dDSm = make_desc(aDS, ATOM, 1024), dKm = make_desc(aK, ATOM, 1024);
-      mbar_wait(kv_full, 0);
-      // S^T(it) = K Q^T and dP^T(it) = V dO^T (reduction over D), committed
+      const uint64_t dDO = make_desc(smem_u32(sDO), 16, 1024), dDOm = make_desc(smem_u32(sDO), ATOM, 1024);
+      // S^T(g) = K Q^T and dP^T(g) = V dO^T (reduction over D), committed
       // separately: the softmax turns S into P while the previous tile's dQ
       // is still being drained from the dP^T columns.
-      auto issue_s = [&](int it) {
-        const int x = it & 1;
+      auto issue_s = [&](int g) {
+        const int x = g & 1;
         const uint64_t dQ = make_desc(smem_u32(sQ + x * Cfg::TILE), 16, 1024);
-        mbar_wait(&q_full[x], (it >> 1) & 1);
+        mbar_wait(&q_full[x], (g >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
@@ -240,14 +300,18 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           tc_mma(tmem + kColS, desc_add(dK, off), desc_add(dQ, off), id_ss, k != 0);
         }
         tc_commit(s_full);
+        BWT(3, g);
       };
-      const uint64_t dDO = make_desc(smem_u32(sDO), 16, 1024), dDOm = make_desc(smem_u32(sDO), ATOM, 1024);
-      auto issue_dp = [&](int it) {
-        if (it > 0) mbar_wait(dq_free, (it - 1) & 1);  // dQ(it-1) out of the dP^T columns
-        BWT(13, it);
-        mbar_wait(do_full, it & 1);
+      // dP^T(g) = V dO^T into the dP^T columns once the drain read dQ(g-1)
+      // (both halves) out of them.
+      auto issue_dp = [&](int g) {
+        mbar_wait(do_full, g & 1);
+        if (g > 0) {
+          mbar_wait(dq_free_h[0], (g - 1) & 1);
+          mbar_wait(dq_free_h[1], (g - 1) & 1);
+        }
         tc_fence_after();
-        BWT(4, it);
+        BWT(4, g);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * ATOM + (k & 3) * 32;
@@ -255,52 +319,76 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         }
         tc_commit(dp_full);
       };
-      // dV(it) += P^T(it) dO(it), P^T from TMEM (queries [0,64) at columns
-      // 0.., [64,128) at 64..), as soon as the softmax warps wrote P^T --
-      // before dS^T(it) exists, so S^T(it+1) can follow right away and the
-      // next tile's P^T overlaps this tile's dS^T.
-      auto issue_dv = [&](int it) {
-        mbar_wait(p_full, it & 1);
+      // dV += P^T(g) dO(g), P^T from TMEM (queries [0,64) at columns 0..,
+      // [64,128) at 64..), as soon as the softmax warps wrote P^T -- before
+      // dS^T(g) exists, so S^T(g+1) can follow right away and the next
+      // tile's P^T overlaps this tile's dS^T.  first: the item's first tile
+      // (overwrite the accumulator).
+      auto issue_dv = [&](int g, bool first) {
+        mbar_wait(p_full, g & 1);
         tc_fence_after();
+        BWT(12, g);
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k)
           tc_mma_ts(tmem + kColDV, tmem + kColS + (k >> 2) * 64 + (k & 3) * 8, desc_add(dDOm, k * 2048), id_kv,
-                    (it | k) != 0);
+                    !(first && k == 0));
         tc_commit(do_empty);
       };
-      issue_s(0);
-      issue_dp(0);
-      issue_dv(0);
-      for (int it = 0; it < n_it; ++it) {
-        const int x = it & 1;
-        const uint64_t dQm = make_desc(smem_u32(sQ + x * Cfg::TILE), ATOM, 1024);
-        // S^T(it+1) over the P^T(it) columns: in order after dV(it), which read them
-        if (it + 1 < n_it) issue_s(it + 1);
-        mbar_wait(ds_full, it & 1);
+      int g = 0, ip = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ip) {
+        const BwItem itm = bw_item(p, w);
+        mbar_wait(kv_full, ip & 1);
         tc_fence_after();
-        BWT(1, it);
-        BWT(3, it);
-        // dK += dS^T Q (reduction over the 128 queries)
+        const int g0 = g;
+        issue_s(g0);
+        issue_dp(g0);
+        if (ip > 0) mbar_wait(dkv_free, (ip - 1) & 1);  // previous item's dK / dV read out of TMEM
+        issue_dv(g0, true);
+        for (int t = 0; t < itm.n_it; ++t, ++g) {
+          const int x = g & 1;
+          const uint64_t dQm = make_desc(smem_u32(sQ + x * Cfg::TILE), ATOM, 1024);
+          // S^T(g+1) over the P^T(g) columns: in order after dV(g), which read them
+          if (t + 1 < itm.n_it) issue_s(g + 1);
+          mbar_wait(ds_full, g & 1);
+          tc_fence_after();
+          BWT(1, g);
+          // dQ = dS K (reduction over the 128 keys; dS^T tile read M-major)
+          // into the dP^T columns, first and in two D halves with their own
+          // commits, so the drain of the first half starts while the second
+          // half and dK run.
+          if constexpr (D == 128) {
 #pragma unroll
-        for (int k = 0; k < T128 / 16; ++k) {
-          const uint32_t offa = (k >> 2) * ATOM + (k & 3) * 32;
-          tc_mma(tmem + Cfg::kColDK, desc_add(dDS, offa), desc_add(dQm, k * 2048), id_kv, (it | k) != 0);
-        }
-        tc_commit(&q_empty[x]);
-        // dQ = dS K (reduction over the 128 keys; dS^T tile read M-major)
+            for (int h = 0; h < 2; ++h) {
 #pragma unroll
-        for (int k = 0; k < T128 / 16; ++k) {
-          tc_mma(tmem + kColDP, desc_add(dDSm, k * 2048), desc_add(dKm, k * 2048), id_dq, k != 0);
+              for (int k = 0; k < T128 / 16; ++k)
+                tc_mma(tmem + kColDP + 64 * h, desc_add(dDSm, k * 2048), desc_add(dKm, h * ATOM + k * 2048),
+                       id_dq_half, k != 0);
+              tc_commit(dq_full_h[h]);
+            }
+          } else {  // D = 64: one N=64 MMA; the drain still reads it in two halves
+#pragma unroll
+            for (int k = 0; k < T128 / 16; ++k)
+              tc_mma(tmem + kColDP, desc_add(dDSm, k * 2048), desc_add(dKm, k * 2048), id_dq, k != 0);
+            tc_commit(dq_full_h[0]);
+            tc_commit(dq_full_h[1]);
+          }
+          // dK += dS^T Q (reduction over the 128 queries)
+#pragma unroll
+          for (int k = 0; k < T128 / 16; ++k) {
+            const uint32_t offa = (k >> 2) * ATOM + (k & 3) * 32;
+            tc_mma(tmem + Cfg::kColDK, desc_add(dDS, offa), desc_add(dQm, k * 2048), id_kv, (t | k) != 0);
+          }
+          tc_commit(&q_empty[x]);
+          tc_commit(pds_free);
+          BWT(2, g);
+          if (t + 1 < itm.n_it) {
+            issue_dp(g + 1);  // after the drain read dQ(g) out of TMEM
+            issue_dv(g + 1, false);
+          }
         }
-        tc_commit(dq_full);
-        tc_commit(pds_free);
-        BWT(2, it);
-        if (it + 1 < n_it) {
-          issue_dp(it + 1);  // after the drain read dQ(it) out of TMEM
-          issue_dv(it + 1);
-        }
+        tc_commit(dkv_done);
+        tc_commit(kv_empty);
       }
-      tc_commit(dkv_done);
     }
   } else if (warp >= 4 && warp < 12) {
     // -------------------------------------------------- P^T / dS^T (key rows)
@@ -309,171 +397,176 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const int half = (warp - 4) >> 2;
     const int r = ew * 32 + lane;
     const uint32_t lb = static_cast<uint32_t>(ew * 32) << 16;
-    for (int it = 0; it < n_it; ++it) {
-      const int qi = i0 + it;
-      float* lse = sLse;
-      float* dl = sDelta;
-      const int64_t vec = (static_cast<int64_t>(b) * p.heads + head) * p.seq + qi * T128;
-      if (it > 0) named_bar(1, 256);  // everyone is done with the previous tile's lse / delta
-      if (half == 0) lse[r] = p.lse2[vec + r];
-      else dl[r] = p.delta[vec + r];
-      named_bar(1, 256);
-      mbar_wait(s_full, it & 1);
-      tc_fence_after();
-      if (warp == 4 && lane == 0) BWT(5, it);
-      const bool diag = p.causal && qi == kj;
-      // Phase A: P^T = 2^(s*scale - lse) from S^T alone; kept in registers
-      // for dS and written back over this half's S^T columns (bf16x2) as the
-      // A operand of dV += P^T dO.
-      float pv[64];
+    int g = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const BwItem itm = bw_item(p, w);
+      for (int t = 0; t < itm.n_it; ++t, ++g) {
+        const float* lse = sLse;
+        const float* dl = sDelta;
+        mbar_wait(lse_full, g & 1);
+        mbar_wait(s_full, g & 1);
+        tc_fence_after();
+        if (warp == 4 && lane == 0) BWT(5, g);
+        const bool diag = p.causal && itm.i0 + t == itm.kj;
+        // Phase A: P^T = 2^(s*scale - lse) from S^T alone; kept in registers
+        // for dS and written back over this half's S^T columns (bf16x2) as
+        // the A operand of dV += P^T dO.
+        float pv[64];
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int c0 = half * 64 + h2 * 32;
-        float sv[32];
-        tmem_ld32(tmem + lb + kColS + c0, sv);
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c0 = half * 64 + h2 * 32;
+          float sv[32];
+          tmem_ld32(tmem + lb + kColS + c0, sv);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int c = c0 + i;
-          pv[h2 * 32 + i] = (diag && c < r) ? 0.f : ex2f(sv[i] * p.scale_log2 - lse[c]);
-        }
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          __nv_bfloat162 hh = __floats2bfloat162_rn(pv[h2 * 32 + 2 * i], pv[h2 * 32 + 2 * i + 1]);
-          pk[i] = *reinterpret_cast<uint32_t*>(&hh);
-        }
-        tmem_st16(tmem + lb + kColS + half * 64 + h2 * 16, pk);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) pv[h2 * 32 + i] *= p.scale;  // dS = (dP - Delta) * (P / sqrt(D))
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);  // P^T in TMEM: dV(it) may start
-      if (warp == 4 && lane == 0) BWT(6, it);
-      // Phase B: dS^T = P^T * (dP^T - Delta) / sqrt(D) once dP^T is in.
-      mbar_wait(dp_full, it & 1);
-      tc_fence_after();
-      if (warp == 4 && lane == 0) BWT(7, it);
-      if (it > 0) mbar_wait(pds_free, (it - 1) & 1);
-      if (warp == 4 && lane == 0) BWT(8, it);
-  // dS^T buffer free (dK(it-1), dQ(it-1) read it)
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int c0 = half * 64 + h2 * 32;
-        float dp[32], ds[32];
-        tmem_ld32(tmem + lb + kColDP + c0, dp);
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 d4 = *reinterpret_cast<const float4*>(dl + c0 + i);
-          ds[i] = pv[h2 * 32 + i] * (dp[i] - d4.x);
-          ds[i + 1] = pv[h2 * 32 + i + 1] * (dp[i + 1] - d4.y);
-          ds[i + 2] = pv[h2 * 32 + i + 2] * (dp[i + 2] - d4.z);
-          ds[i + 3] = pv[h2 * 32 + i + 3] * (dp[i + 3] - d4.w);
-        }
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint4 ud;
-          __nv_bfloat162* hd = reinterpret_cast<__nv_bfloat162*>(&ud);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) hd[i] = __floats2bfloat162_rn(ds[8 * g + 2 * i], ds[8 * g + 2 * i + 1]);
-          *reinterpret_cast<uint4*>(sDS + swz(r, c0 / 8 + g)) = ud;
-        }
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
-      if (warp == 4 && lane == 0) BWT(9, it);
-    }
-    // dK, dV rows of this key tile -> dqkv.
-    mbar_wait(dkv_done, 0);
-    tc_fence_after();
-    const int64_t row = static_cast<int64_t>(b) * p.seq + kj * T128 + r;
-    __nv_bfloat16* out = p.dqkv + row * 3 * p.hidden + head * D;
-    {
-      const int part = half;  // half 0 writes dK, half 1 writes dV
-      const uint32_t col = part ? kColDV : Cfg::kColDK;
-      __nv_bfloat16* dst = out + (part ? 2 : 1) * p.hidden;
-#pragma unroll
-      for (int c = 0; c < D; c += 32) {
-        float v[32];
-        tmem_ld32(tmem + lb + col + c, v);
-#pragma unroll
-        for (int g = 0; g < 32; g += 8) {
-          uint4 u;
-          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(v[g + 2 * i], v[g + 2 * i + 1]);
-          *reinterpret_cast<uint4*>(dst + c + g) = u;
-        }
-        if (p.dbias) {
-          // bias gradient: column sums of this warp's 32 key rows (a
-          // transposing butterfly leaves column c + lane in v[0]), one
-          // atomic per column per warp
-#pragma unroll
-          for (int sh = 16; sh >= 1; sh >>= 1) {
-            const bool up = (lane & sh) != 0;
-#pragma unroll
-            for (int i = 0; i < sh; ++i) {
-              const float send = up ? v[i] : v[i + sh];
-              const float keep = up ? v[i + sh] : v[i];
-              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
-            }
+          for (int i = 0; i < 32; ++i) {
+            const int c = c0 + i;
+            pv[h2 * 32 + i] = (diag && c < r) ? 0.f : ex2f(sv[i] * p.scale_log2 - lse[c]);
           }
-          atomicAdd(p.dbias + (part ? 2 : 1) * p.hidden + head * D + c + lane, v[0]);
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            __nv_bfloat162 hh = __floats2bfloat162_rn(pv[h2 * 32 + 2 * i], pv[h2 * 32 + 2 * i + 1]);
+            pk[i] = *reinterpret_cast<uint32_t*>(&hh);
+          }
+          tmem_st16(tmem + lb + kColS + half * 64 + h2 * 16, pk);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) pv[h2 * 32 + i] *= p.scale;  // dS = (dP - Delta) * (P / sqrt(D))
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);  // P^T in TMEM: dV(g) may start
+        if (warp == 4 && lane == 0) BWT(6, g);
+        // Phase B: dS^T = P^T * (dP^T - Delta) / sqrt(D) once dP^T is in.
+        mbar_wait(dp_full, g & 1);
+        mbar_wait(dl_full, g & 1);
+        tc_fence_after();
+        if (warp == 4 && lane == 0) BWT(7, g);
+        if (g > 0) mbar_wait(pds_free, (g - 1) & 1);  // dS^T buffer free (dK(g-1), dQ(g-1) read it)
+        if (warp == 4 && lane == 0) BWT(8, g);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c0 = half * 64 + h2 * 32;
+          float dp[32], ds[32];
+          tmem_ld32(tmem + lb + kColDP + c0, dp);
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 d4 = *reinterpret_cast<const float4*>(dl + c0 + i);
+            ds[i] = pv[h2 * 32 + i] * (dp[i] - d4.x);
+            ds[i + 1] = pv[h2 * 32 + i + 1] * (dp[i + 1] - d4.y);
+            ds[i + 2] = pv[h2 * 32 + i + 2] * (dp[i + 2] - d4.z);
+            ds[i + 3] = pv[h2 * 32 + i + 3] * (dp[i + 3] - d4.w);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 ud;
+            __nv_bfloat162* hd = reinterpret_cast<__nv_bfloat162*>(&ud);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) hd[i] = __floats2bfloat162_rn(ds[8 * q + 2 * i], ds[8 * q + 2 * i + 1]);
+            *reinterpret_cast<uint4*>(sDS + swz(r, c0 / 8 + q)) = ud;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ds_full);
+        if (warp == 4 && lane == 0) BWT(9, g);
       }
     }
   } else if (warp >= 12) {
-    // ------------------------------------------------ dQ drain (query rows)
+    // ----------------------------- dQ drain (query rows) and dK / dV epilogue
     // TMEM -> fp32 SW128 slabs (two per warp, in their own buffer) -> TMA
     // bulk reduce-add into dq_acc: whole 128-byte row segments reduced in L2
     // instead of per-lane atomics.  The row is read out of TMEM in two halves
     // and dq_free is raised as soon as the second half is in registers, so
-    // the next dP^T overlaps the reduce-adds.
+    // the next dP^T overlaps the reduce-adds.  After an item's last tile the
+    // same warps write its dK / dV rows (and the K / V bias-gradient column
+    // sums), then free those TMEM columns for the next item.
     const int ew = warp & 3;
     const uint32_t lb = static_cast<uint32_t>(ew * 32) << 16;
     uint8_t* slabs = sStage + ew * 2 * SLAB_BYTES;
     constexpr int NCH = D / 32, HALF = NCH / 2;
-    for (int it = 0; it < n_it; ++it) {
-      const int qi = i0 + it;
-      mbar_wait(dq_full, it & 1);
-      tc_fence_after();
-      if (warp == 12 && lane == 0) BWT(10, it);
-      const int row0 = b * p.seq + qi * T128 + ew * 32;
+    int g = 0, ip = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ip) {
+      const BwItem itm = bw_item(p, w);
+      for (int t = 0; t < itm.n_it; ++t, ++g) {
+        const int qi = itm.i0 + t;
+        const int row0 = itm.b * p.seq + qi * T128 + ew * 32;
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        uint32_t u[HALF][32];
+        for (int h = 0; h < 2; ++h) {  // D half h of dQ (its own MMA commit)
+          mbar_wait(dq_full_h[h], g & 1);
+          tc_fence_after();
+          if (h == 0 && warp == 12 && lane == 0) BWT(10, g);
+          uint32_t u[HALF][32];
 #pragma unroll
-        for (int c = 0; c < HALF; ++c) tmem_ld32_issue(tmem + lb + kColDP + (r * HALF + c) * 32, u[c]);
-        tmem_wait_ld();
-        float v[HALF][32];
-#pragma unroll
-        for (int c = 0; c < HALF; ++c)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[c][i] = __uint_as_float(u[c][i]);
-        if (r == 1) {
+          for (int c = 0; c < HALF; ++c) tmem_ld32_issue(tmem + lb + kColDP + (h * HALF + c) * 32, u[c]);
+          tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(dq_free);  // dQ TMEM columns read out
-          if (warp == 12 && lane == 0) BWT(11, it);
-        }
+          if (lane == 0) mbar_arrive(dq_free_h[h]);  // these dQ columns read out: dP^T half h may start
+          if (h == 1 && warp == 12 && lane == 0) BWT(11, g);
+          float v[HALF][32];
 #pragma unroll
-        for (int c = 0; c < HALF; ++c) {
-          uint8_t* sb = slabs + ((r * HALF + c) & 1) * SLAB_BYTES;
-          if (lane == 0) bulk_wait_read<1>();
-          __syncwarp();
-          slab_put_f32(sb, lane, v[c]);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_reduce_add_2d(&map_dq, sb, head * D + (r * HALF + c) * 32, row0);
-            bulk_commit();
+          for (int c = 0; c < HALF; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[c][i] = __uint_as_float(u[c][i]);
+#pragma unroll
+          for (int c = 0; c < HALF; ++c) {
+            uint8_t* sb = slabs + ((h * HALF + c) & 1) * SLAB_BYTES;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            slab_put_f32(sb, lane, v[c]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_reduce_add_2d(&map_dq, sb, itm.head * D + (h * HALF + c) * 32, row0);
+              bulk_commit();
+            }
           }
         }
       }
+      // dK, dV rows of this key tile -> dqkv.
+      mbar_wait(dkv_done, ip & 1);
+      tc_fence_after();
+      const int64_t row = static_cast<int64_t>(itm.b) * p.seq + itm.kj * T128 + ew * 32 + lane;
+      __nv_bfloat16* out = p.dqkv + row * 3 * p.hidden + itm.head * D;
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {  // 0: dK, 1: dV
+        const uint32_t col = part ? kColDV : Cfg::kColDK;
+        __nv_bfloat16* dst = out + (part ? 2 : 1) * p.hidden;
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          float v[32];
+          tmem_ld32(tmem + lb + col + c, v);
+#pragma unroll
+          for (int q = 0; q < 32; q += 8) {
+            uint4 u;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(v[q + 2 * i], v[q + 2 * i + 1]);
+            *reinterpret_cast<uint4*>(dst + c + q) = u;
+          }
+          if (p.dbias) {
+            // bias gradient: column sums of this warp's 32 key rows (a
+            // transposing butterfly leaves column c + lane in v[0]), one
+            // atomic per column per warp
+#pragma unroll
+            for (int sh = 16; sh >= 1; sh >>= 1) {
+              const bool up = (lane & sh) != 0;
+#pragma unroll
+              for (int i = 0; i < sh; ++i) {
+                const float send = up ? v[i] : v[i + sh];
+                const float keep = up ? v[i + sh] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+              }
+            }
+            atomicAdd(p.dbias + (part ? 2 : 1) * p.hidden + itm.head * D + c + lane, v[0]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dkv_free);
     }
     if (lane == 0) bulk_wait<0>();
   }
@@ -601,10 +694,12 @@ void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const flo
   p.dbias = dbias;
   static const int group = [] {
     const char* g = std::getenv("WP_BW_GROUP");  // A/B switch; 0 = one group
-    return g ? std::atoi(g) : 0;
+    return g ? std::atoi(g) : 32;
   }();
   p.group = group;
-  const int grid = p.n_tiles * s.heads * s.mbs;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::min(p.n_tiles * s.heads * s.mbs, sms);  // persistent: one CTA per SM
   const CUtensorMap mdq = make_slab_map(dq_acc, kF32, s.hidden, int64_t(s.mbs) * s.seq, s.hidden);
   k<<<grid, BW_THREADS, BwCfg<D>::SMEM, stream>>>(mq, mk, mv, mdo, mdq, p);
   const cudaError_t e = cudaGetLastError();
@@ -635,6 +730,7 @@ int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const v
 }
 
 }  // namespace wpk
+
 
 #ifdef WP_BW_TRACE
 extern "C" int wp_debug_bw_trace(unsigned long long* out, int n) {

@@ -243,4 +243,6 @@ def test_device_inputs_ordered_after_producer_stream():
         lab.copy_(torch.from_numpy(labels).pin_memory(), non_blocking=True)
         got = rt.train_step(tok, lab)      # the producer is torch's current stream here
     del big
-    assert got == want
+    # zeros (an unordered read) would give a different loss; equal up to the
+    # run-to-run rounding of the fp32 reductions otherwise
+    assert abs(got - want) <= 1e-6 * abs(want), (got, want)
