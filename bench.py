@@ -397,12 +397,19 @@ def main():
     rt.set_tracing(False)
     tr = rt.trace()
     if world > 1:
-        # replica 0's pipeline devices make up the measured trace of the list
+        # replica 0's pipeline devices make up the measured trace of the list;
+        # each rank's trace starts at its own step begin, so put them on one
+        # device clock (%globaltimer at each rank's step begin) before merging
         pipe = rank % P
-        mine = (tr.intervals[pipe], [e for e in tr.comm_events if e.src_device == pipe])
+        mine = (tr.intervals[pipe], [e for e in tr.comm_events if e.src_device == pipe], rt.step_clock_ns())
         parts = [None] * world
         dist.all_gather_object(parts, mine)
-        tr = wp.build_trace([p[0] for p in parts[:P]], [e for p in parts[:P] for e in p[1]])
+        t0 = min(p[2] for p in parts[:P])
+        off = [(p[2] - t0) * 1e-9 for p in parts[:P]]
+        tr = wp.build_trace([[iv._replace(start=iv.start + off[d], end=iv.end + off[d]) for iv in parts[d][0]]
+                             for d in range(P)],
+                            [e._replace(post_time=e.post_time + off[d], arrival_time=e.arrival_time + off[d])
+                             for d in range(P) for e in parts[d][1]])
     measured_bubble = wp.bubble_ratio(tr)
     pool_b, landing_b = rt.memory()
     mem = [None] * world
@@ -479,6 +486,7 @@ def main():
         "config": workload_config(args, world),
         "tc_peak_frac": flops_step * args.steps / sec / world / (peak_tc * 1e12),
         "bubble": {"measured": measured_bubble, "simulated_at_measured_costs": sim_bubble, "eq1": eq1,
+                   "clock": "per-rank traces aligned on %globaltimer at step begin" if world > 1 else "one device",
                    "t_forward_s": tf, "t_backward_s": tb},
         "p2p": p2p,
         "memory": {"stash_pool_gb_max": max(m[0] for m in mem) / 1e9,

@@ -128,7 +128,8 @@ int wp_trace_to_gantt(const wp_trace* trace, const char* format, char** out);
 int wp_compare(const int* schemes, const int* waves, int n, int budget_devices, int microbatches,
                const wp_cost* base_cost, int format, char** out);
 int wp_compare_measured(const int* schemes, const int* waves, int n, int budget_devices, int microbatches,
-                        const wp_trace* const* traces, const wp_list* const* lists, int format, char** out);
+                        const wp_trace* const* traces, const wp_list* const* lists, double t_comm, int format,
+                        char** out);
 
 /* bubble_ratio, src/analytics.cpp:32-46. */
 int wp_bubble_ratio(const wp_trace* trace, double* out);
@@ -220,6 +221,11 @@ int wp_train_step_stream(wp_runtime* rt, const int32_t* tokens, const int32_t* l
                          void* producer_stream, float* loss);
 int wp_runtime_set_stall_timeout(wp_runtime* rt, double seconds);
 int wp_runtime_trace(wp_runtime* rt, const wp_trace** trace);
+/* %globaltimer (ns) on the device when the last traced step began -- the
+ * origin of that step's measured trace.  Ranks of a multi-process job shift
+ * their traces by (their value - the smallest) before merging them
+ * (wp_trace_build), so the merged trace is on one device clock. */
+int wp_runtime_step_clock(const wp_runtime* rt, int64_t* ns);
 /* Enables per-action CUDA events (measured trace); off = no event overhead. */
 int wp_runtime_set_tracing(wp_runtime* rt, int enabled);
 /* Skip the optimizer update (gradients stay accumulated); for parity tests. */

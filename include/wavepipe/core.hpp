@@ -310,10 +310,11 @@ std::vector<CompareRow> compare(const std::vector<CompareRequest>& requests, int
 // The same rows from MEASURED traces (the GPU runtime's train_step, one per
 // request, traces[i] of lists[i]): makespan = measured step (seconds),
 // simulated_ratio = bubble_ratio of the measured trace; Hanayo's analytic
-// ratio at the measured mean slice costs.  Same order and writers.
+// ratio at the measured mean slice costs and the given (measured) message
+// latency t_comm.  Same order and writers.
 std::vector<CompareRow> compare_measured(const std::vector<CompareRequest>& requests, int budget_devices,
                                          int microbatches, const std::vector<SimTrace>& traces,
-                                         const std::vector<ActionList>& lists);
+                                         const std::vector<ActionList>& lists, double t_comm = 0.0);
 std::string compare_to_csv(const std::vector<CompareRow>& rows);
 std::string compare_to_json(const std::vector<CompareRow>& rows);
 

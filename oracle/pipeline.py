@@ -1,17 +1,17 @@
 """CPU interpreter of an action list with real message passing -- TEST ORACLE.
 
-Executes each pipeline device's program in order, exactly as the runtime's
-NCCL transport issues it (paper_2308_15762_b200/csrc/runtime/executor.cpp,
+Executes each pipeline device's program in order, as the runtime's action
+interpreter does (paper_2308_15762_b200/csrc/runtime/executor.cpp,
 Runtime::advance): Forward/Backward run the slice's units with torch autograd
 on CPU; Send/Receive are point-to-point messages; a BatchedExchange is one
 grouped send+recv with its counterpart.  The slice->unit partition restates
-partition_units (csrc/runtime/model.cpp).
+the runtime's device-balanced partition_units (csrc/runtime/model.cpp).
 
 Drivers: `run_local` (all devices in one process, relaxation order like the
 reference simulator, src/simulate.cpp:86-158) and `run_dist` (one process
 per device over torch.distributed point-to-point; the gloo world_size-2
-test).  `channels` gives the per-directed-pair sender order the runtime's
-NCCL transport posts its receives in.
+test).  `channels` gives the per-directed-pair sender order `run_dist`
+posts its receives in (gloo matches a pair's messages FIFO).
 """
 import torch
 
@@ -32,25 +32,75 @@ def units(desc):
     return u
 
 
-def partition(us, S):
-    """partition_units (csrc/runtime/model.cpp)."""
-    N = len(us)
+def partition(us, slice_device, P):
+    """partition_units(units, slice_device, P) (csrc/runtime/model.cpp): the
+    device-balanced cut the runtime uses.  Per-slice targets give every device
+    total/P (the pinned embedding / LM head counting toward their device),
+    cuts are placed greedily on those targets, then a coordinate descent moves
+    each cut to the position minimising (busiest device load, sum of squared
+    device loads) until no cut moves.  Numerics do not depend on the cut
+    (pipelined = sequential for any partition); the interpreter uses it so it
+    executes the runtime's slices unit for unit."""
+    S, N = len(slice_device), len(us)
     prefix = [0.0]
     for _, _, c in us:
         prefix.append(prefix[-1] + c)
-    total = prefix[-1]
+    total = prefix[N]
+    fixed = [0.0] * S
+    fixed[0] += us[0][2]
+    fixed[S - 1] += us[-1][2]
+    dev_fixed, dev_slices = [0.0] * P, [0] * P
+    for k in range(S):
+        dev_fixed[slice_device[k]] += fixed[k]
+        dev_slices[slice_device[k]] += 1
+    target = [fixed[k] + max(0.0, total / P - dev_fixed[slice_device[k]]) / dev_slices[slice_device[k]]
+              for k in range(S)]
+    tsum = sum(target)
     b = [0] * (S + 1)
     b[S] = N
+    cum = 0.0
     for k in range(1, S):
-        target = total * k / S
+        cum += target[k - 1] * total / tsum
         lo = max(b[k - 1], 1)
-        best, best_d = lo, abs(prefix[lo] - target)
+        best, best_d = lo, abs(prefix[lo] - cum)
         for i in range(lo + 1, N):
-            d = abs(prefix[i] - target)
+            d = abs(prefix[i] - cum)
             if d < best_d:
                 best, best_d = i, d
         b[k] = min(best, N - 1)
+
+    def score(bb):
+        load = [0.0] * P
+        for k in range(S):
+            load[slice_device[k]] += prefix[bb[k + 1]] - prefix[bb[k]]
+        return max(load), sum(x * x for x in load)
+
+    cur = score(b)
+    moved = True
+    while moved:
+        moved = False
+        for k in range(1, S):
+            lo, hi = max(b[k - 1], 1), min(b[k + 1], N - 1)
+            best, best_s = b[k], cur
+            for pos in range(lo, hi + 1):
+                b[k] = pos
+                sc = score(b)
+                if sc < best_s:
+                    best_s, best = sc, pos
+            b[k] = best
+            if best_s < cur:
+                cur = best_s
+                moved = True
     return b
+
+
+def slice_devices(placement):
+    S = sum(len(r) for r in placement)
+    sd = [0] * S
+    for d, row in enumerate(placement):
+        for s in row:
+            sd[s] = d
+    return sd
 
 
 def key_of(a):
@@ -64,9 +114,8 @@ def channels(per_device):
     """Directed device pairs (src, dst) with their messages in the SENDER's
     program order (Sends and the outgoing halves of BatchedExchanges).
 
-    The runtime's NCCL transport gives every directed pair its own
-    communicator; the receiver posts its receives for a channel in this
-    sender order at step start (so NCCL's FIFO matching pairs each message
+    run_dist's receiver posts its receives for a channel in this sender
+    order at step start (so the FIFO matching of point-to-point pairs each message
     with the right landing buffer even where the receiver consumes messages
     in another order -- per-pair program orders differ, e.g. activations and
     gradients interleave differently on the two sides)."""
@@ -166,9 +215,8 @@ def owner(placement, s):
 
 def run_local(desc, params, per_device, placement, B, tokens, labels):
     """Single process, all devices, relaxation order (as src/simulate.cpp)."""
-    S = sum(len(r) for r in placement)
     us = units(desc)
-    bounds = partition(us, S)
+    bounds = partition(us, slice_devices(placement), len(placement))
     devs = [Device(desc, params, placement[d], bounds, us) for d in range(len(per_device))]
     published = {}
     pc = [0] * len(devs)
@@ -210,8 +258,7 @@ def run_local(desc, params, per_device, placement, B, tokens, labels):
 
 def run_dist(desc, params, per_device, placement, B, tokens, labels, replicas=1):
     """One process per pipeline device over torch.distributed point-to-point
-    (gloo on CPU), issuing communication the way the runtime's NCCL transport
-    does: every incoming message of the step is posted at step start, per
+    (gloo on CPU): every incoming message of the step is posted at step start, per
     channel in the sender's order (FIFO matching, tag 0); Sends and the
     outgoing halves of BatchedExchanges are issued in program order right
     after their producer; a consumer waits only for its own message.
@@ -225,9 +272,8 @@ def run_dist(desc, params, per_device, placement, B, tokens, labels, replicas=1)
     P = len(per_device)
     g = dist.get_rank()
     r, base = g % P, (g // P) * P
-    S = sum(len(x) for x in placement)
     us = units(desc)
-    bounds = partition(us, S)
+    bounds = partition(us, slice_devices(placement), len(placement))
     dev = Device(desc, params, placement[r], bounds, us)
     shape = (desc.micro_batch_size, desc.seq, desc.hidden)
     pending = {}

@@ -86,7 +86,7 @@ _SIGS = {
     "wp_trace_build": (I, [I, IP, C.POINTER(wp_interval), I, C.POINTER(wp_comm_event), PP]),
     "wp_trace_to_gantt": (I, [P, C.c_char_p, C.POINTER(C.c_void_p)]),
     "wp_compare": (I, [IP, IP, I, I, I, C.POINTER(wp_cost), I, C.POINTER(C.c_void_p)]),
-    "wp_compare_measured": (I, [IP, IP, I, I, I, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), I,
+    "wp_compare_measured": (I, [IP, IP, I, I, I, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), D, I,
                                 C.POINTER(C.c_void_p)]),
     "wp_bubble_ratio": (I, [P, DP]),
     "wp_memory_profile": (I, [P, P, I64P, I64P]),
@@ -103,6 +103,7 @@ _SIGS = {
     "wp_runtime_set_stall_timeout": (I, [P, D]),
     "wp_runtime_trace": (I, [P, PP]),
     "wp_runtime_set_tracing": (I, [P, I]),
+    "wp_runtime_step_clock": (I, [P, I64P]),
     "wp_runtime_set_update": (I, [P, I]),
     "wp_param_count": (I, [P, IP]),
     "wp_param_info": (I, [P, I, C.POINTER(C.c_char_p), I64P, IP]),

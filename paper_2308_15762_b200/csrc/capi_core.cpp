@@ -245,7 +245,8 @@ int wp_compare(const int* schemes, const int* waves, int n, int budget_devices, 
 }
 
 int wp_compare_measured(const int* schemes, const int* waves, int n, int budget_devices, int microbatches,
-                        const wp_trace* const* traces, const wp_list* const* lists, int format, char** out) {
+                        const wp_trace* const* traces, const wp_list* const* lists, double t_comm, int format,
+                        char** out) {
   try {
     if ((n > 0 && (!schemes || !waves || !traces || !lists)) || !out) return fail(WP_ERR_CONFIG, "null argument");
     std::vector<wavepipe::SimTrace> tr;
@@ -255,7 +256,8 @@ int wp_compare_measured(const int* schemes, const int* waves, int n, int budget_
       tr.push_back(traces[i]->trace);
       ls.push_back(lists[i]->list);
     }
-    const auto rows = wavepipe::compare_measured(requests_of(schemes, waves, n), budget_devices, microbatches, tr, ls);
+    const auto rows = wavepipe::compare_measured(requests_of(schemes, waves, n), budget_devices, microbatches, tr, ls,
+                                                 t_comm);
     *out = dup_c(format == 1 ? wavepipe::compare_to_json(rows) : wavepipe::compare_to_csv(rows));
     return WP_OK;
   } catch (...) {

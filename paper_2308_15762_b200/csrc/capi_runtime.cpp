@@ -144,6 +144,12 @@ int wp_runtime_trace(wp_runtime* rt, const wp_trace** trace) {
   return WP_OK;
 }
 
+int wp_runtime_step_clock(const wp_runtime* rt, int64_t* ns) {
+  if (!rt || !ns) return fail(WP_ERR_CONFIG, "null argument");
+  *ns = rt->rt->step_clock_ns();
+  return WP_OK;
+}
+
 int wp_runtime_set_tracing(wp_runtime* rt, int enabled) {
   if (!rt) return fail(WP_ERR_CONFIG, "null argument");
   rt->rt->set_tracing(enabled != 0);

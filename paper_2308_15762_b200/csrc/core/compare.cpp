@@ -105,7 +105,7 @@ std::vector<CompareRow> compare(const std::vector<CompareRequest>& requests, int
 
 std::vector<CompareRow> compare_measured(const std::vector<CompareRequest>& requests, int budget_devices,
                                          int microbatches, const std::vector<SimTrace>& traces,
-                                         const std::vector<ActionList>& lists) {
+                                         const std::vector<ActionList>& lists, double t_comm) {
   if (traces.size() != requests.size() || lists.size() != requests.size()) {
     throw std::invalid_argument("compare_measured: one trace and one list per request");
   }
@@ -134,7 +134,7 @@ std::vector<CompareRow> compare_measured(const std::vector<CompareRequest>& requ
         if (nf && nb) {
           row.has_analytic = true;
           row.analytic_ratio = analytic_bubble_hanayo_d(cfg.devices, cfg.waves, 2.0 * cfg.waves * f / nf,
-                                                        2.0 * cfg.waves * b / nb, 0.0);
+                                                        2.0 * cfg.waves * b / nb, t_comm);
         }
       }
       for (const Rational& w : m.memory.weight_units) row.weight_units = std::max(row.weight_units, w);

@@ -1041,6 +1041,18 @@ int softmax_bwd(int dtype, const float* dP, void* P, int rows, int n, float scal
   return 1;
 }
 
+__global__ void stamp_globaltimer_k(uint64_t* out) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+
+int stamp_globaltimer(uint64_t* out, cudaStream_t s) {
+  stamp_globaltimer_k<<<1, 1, 0, s>>>(out);
+  check_launch("stamp_globaltimer");
+  return 1;
+}
+
 int wait_flag(cudaStream_t s, const uint32_t* flag, uint32_t epoch, const uint32_t* abort_word) {
   wait_flag_k<<<1, 1, 0, s>>>(flag, epoch, abort_word);
   check_launch("wait_flag");

@@ -74,6 +74,10 @@ int allreduce_scaled_peers(float* const* bufs, int G, int me, int64_t n, float s
 // acquire load at system scope orders the peer's bytes before what follows.
 int wait_flag(cudaStream_t s, const uint32_t* flag, uint32_t epoch, const uint32_t* abort_word);
 
+// *out = %globaltimer (ns) when the stream reaches this point: the common
+// device clock that aligns the measured traces of the ranks of a job.
+int stamp_globaltimer(uint64_t* out, cudaStream_t s);
+
 // Deterministic N(0, std) init from a counter-based hash (Box-Muller).
 int init_normal(float* p, int64_t n, float std, uint64_t seed, cudaStream_t s);
 int fill_f32(float* p, int64_t n, float v, cudaStream_t s);

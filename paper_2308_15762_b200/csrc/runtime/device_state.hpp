@@ -54,6 +54,8 @@ struct DeviceState {
   // removed when its backward is; the high-water mark over all steps, and
   // per slice the largest entry seen.
   int64_t live_stash = 0, peak_stash = 0;
+  uint64_t* clock_host = nullptr;  // mapped pinned word: %globaltimer at the traced step's begin
+  uint64_t* clock_dev = nullptr;
   std::map<int, int64_t> slice_stash_bytes;
   bool dy_bias_done = false;    // the incoming dy's column sums are already in this unit's bias grad
   std::vector<std::pair<int, int>> be_partner;  // per position: (device, position) of a BE's counterpart

@@ -12,6 +12,8 @@
 #include <stdexcept>
 #include <thread>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "capi_internal.hpp"
 #include "kernels/attention.cuh"
 #include "runtime/device_state.hpp"
@@ -178,6 +180,7 @@ Runtime::~Runtime() {
                     static_cast<void*>(d->ln_rows)})
       if (p) cudaFree(p);
     d->pool.reset();
+    if (d->clock_host) cudaFreeHost(d->clock_host);
     if (d->compute) cudaStreamDestroy(d->compute);
     if (d->copy) cudaStreamDestroy(d->copy);
     for (auto& kv : d->tx) cudaStreamDestroy(kv.second);
@@ -1084,12 +1087,34 @@ void Runtime::optimizer(DeviceState& d) {
   });
 }
 
+// NVTX range per enqueued action ("dev 2 Forward mb 3 slice 5"), for
+// timeline tools (nsys / ncu --nvtx); a no-op unless a tool is attached.
+struct NvtxAction {
+  bool on;
+  NvtxAction(int dev, const Action& a) : on(nvtx_active()) {
+    if (!on) return;
+    char buf[96];
+    std::snprintf(buf, sizeof buf, "dev %d %s mb %d slice %d", dev, wavepipe::action_kind_name(a.kind), a.microbatch,
+                  a.slice_index);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxAction() {
+    if (on) nvtxRangePop();
+  }
+  static bool nvtx_active() {
+    static const bool active = std::getenv("NSYS_PROFILING_SESSION_ID") || std::getenv("NVTX_INJECTION64_PATH") ||
+                               std::getenv("WP_NVTX");
+    return active;
+  }
+};
+
 bool Runtime::advance(DeviceState& d) {
   const auto& prog = list_.per_device[d.pipe];
   bool moved = false;
   DevGuard g(d.cuda);
   while (d.pc < prog.size()) {
     const Action& a = prog[d.pc];
+    NvtxAction range(d.pipe, a);
     if (a.is_compute()) {
       for (cudaEvent_t e : d.pending) ck(cudaStreamWaitEvent(d.compute, e, 0), "wait arrival");
       d.pending.clear();
@@ -1220,6 +1245,15 @@ float Runtime::train_step(const int32_t* tokens, const int32_t* labels, bool on_
     d->starts.clear();
     d->published_at.assign(list_.per_device[d->pipe].size(), 0);
     ck(cudaEventRecord(d->step_begin, d->compute), "record step begin");
+    if (tracing_) {
+      if (!d->clock_host) {
+        void* mem = nullptr;
+        ck(cudaHostAlloc(&mem, sizeof(uint64_t), cudaHostAllocMapped), "cudaHostAlloc clock word");
+        d->clock_host = static_cast<uint64_t*>(mem);
+        ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d->clock_dev), mem, 0), "clock word device pointer");
+      }
+      launches_ += wpk::stamp_globaltimer(d->clock_dev, d->compute);  // right after step_begin
+    }
     ck(cudaStreamWaitEvent(d->copy, d->step_begin, 0), "copy after begin");
   }
   enqueue_step();
@@ -1360,6 +1394,7 @@ void Runtime::stalled() {
 }
 
 void Runtime::collect_trace() {
+  step_clock_ns_ = devs_.front()->clock_host ? static_cast<int64_t>(*devs_.front()->clock_host) : 0;
   trace_ = wavepipe::SimTrace{};
   trace_.intervals.resize(list_.config.devices);
   auto rel = [](DeviceState* d, cudaEvent_t e) {

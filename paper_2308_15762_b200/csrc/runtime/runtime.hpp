@@ -141,6 +141,10 @@ class Runtime {
   void set_stall_timeout(double seconds) { stall_timeout_s_ = seconds; }
 
   const wavepipe::SimTrace& trace() const { return trace_; }
+  // %globaltimer (ns) on the (first local) device when the last traced step
+  // began: trace times are relative to it, so adding it puts the ranks of
+  // a job on one device clock.
+  int64_t step_clock_ns() const { return step_clock_ns_; }
   void set_tracing(bool on) { tracing_ = on; }
   void set_update(bool on) { update_ = on; }
   // Per-GEMM CUDA events on the launching (compute) stream; accumulated over
@@ -260,6 +264,7 @@ class Runtime {
   std::map<std::string, ShapeStat> prof_shapes_;
   std::map<std::string, ShapeStat> hbm_stats_;  // flops field = bytes
   double stall_timeout_s_ = 300.0;
+  int64_t step_clock_ns_ = 0;
   bool broken_ = false;    // a stalled step left the runtime unusable
   bool released_ = false;  // ... and its device waits were released (safe to free)
   cudaEvent_t input_ready_ = nullptr;

@@ -1,10 +1,12 @@
-// CUDA stream memory operations (cuStreamWaitValue32 / cuStreamWriteValue32),
-// bound through the runtime's driver entry-point query so libwavepipe.so keeps
-// linking only the static CUDA runtime.
+// CUDA stream memory write (cuStreamWriteValue32), bound through the
+// runtime's driver entry-point query so libwavepipe.so keeps linking only the
+// static CUDA runtime.
 //
-// These are the IPC transport's device-side signals: a 32-bit flag written by
-// one GPU's stream (after a copy-engine transfer) and waited on by another
-// GPU's stream, with no host round trip and no SM spin kernel.
+// The IPC transport's device-side signals: a 32-bit flag written by one
+// GPU's stream (after a copy-engine transfer, no host round trip).  The
+// waiting side is a bounded wait kernel (wpk::wait_flag), not
+// cuStreamWaitValue32: a memory-op wait on a peer that never signals cannot
+// be released, a wait kernel can (see the stall watchdog).
 #pragma once
 
 #include <cuda.h>
@@ -18,7 +20,6 @@
 namespace wprt {
 
 struct StreamOps {
-  CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
   CUresult (*write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
 
   static const StreamOps& get() {
@@ -33,19 +34,12 @@ struct StreamOps {
           error = std::string("driver entry point ") + name + " unavailable";
         }
       };
-      bind("cuStreamWaitValue32", reinterpret_cast<void**>(&ops.wait32));
       bind("cuStreamWriteValue32", reinterpret_cast<void**>(&ops.write32));
     });
     if (!error.empty()) throw std::runtime_error(error);
     return ops;
   }
 
-  // Stream waits until *flag >= value (wrap-free: epochs are < 2^31 apart).
-  static void wait_geq(cudaStream_t s, const uint32_t* flag, uint32_t value) {
-    const CUresult r = get().wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value,
-                                    CU_STREAM_WAIT_VALUE_GEQ);
-    if (r != CUDA_SUCCESS) throw std::runtime_error("cuStreamWaitValue32 failed: " + std::to_string(r));
-  }
   // Stream writes *flag = value once all earlier work of the stream is done;
   // the default flags include a memory barrier, so the earlier transfer's
   // bytes are visible to whoever observes the flag.

@@ -158,6 +158,12 @@ class Runtime:
         check(lib.wp_runtime_trace(self._h, C.byref(p)))
         return SimTrace(p, owned=False)
 
+    def step_clock_ns(self):
+        """%globaltimer (ns) when the last traced step began (its trace's origin)."""
+        n = C.c_int64()
+        check(lib.wp_runtime_step_clock(self._h, C.byref(n)))
+        return n.value
+
     def launch_count(self):
         n = C.c_int64()
         check(lib.wp_runtime_launch_count(self._h, C.byref(n)))

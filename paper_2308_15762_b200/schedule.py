@@ -85,6 +85,12 @@ class CostModel:
         wave = cfg.scheme in (Scheme.Hanayo, Scheme.ChimeraWave)
         return self.t_backward / (2.0 * cfg.waves) if wave else self.t_backward
 
+    def rescaled(self, budget_devices, config_devices):
+        """ref include/wavepipe/cost_model.hpp:42-48: compute costs scaled by
+        budget/config devices (one chimera-wave group of a budget)."""
+        k = budget_devices / config_devices
+        return CostModel(self.t_forward * k, self.t_backward * k, self.t_comm)
+
 
 class Action(NamedTuple):
     kind: ActionKind
@@ -290,15 +296,16 @@ def compare(requests, budget_devices, microbatches, cost: CostModel = None, fmt:
                          fmt)
 
 
-def compare_measured(requests, budget_devices, microbatches, traces, lists, fmt: str = "json") -> str:
+def compare_measured(requests, budget_devices, microbatches, traces, lists, t_comm=0.0, fmt: str = "json") -> str:
     """The same rows from measured traces (one per request, e.g. the GPU
     runtime's train_step traces of lists[i]): makespan in seconds, the
-    bubble ratio of the measured trace."""
+    bubble ratio of the measured trace, Hanayo's Eq. 1 at the measured mean
+    slice costs and message latency t_comm."""
     n, sch, wav = _requests(requests)
     tr = (C.c_void_p * max(n, 1))(*[t._h for t in traces])
     ls = (C.c_void_p * max(n, 1))(*[x.handle for x in lists])
-    return _compare_text(lambda f, o: lib.wp_compare_measured(sch, wav, n, budget_devices, microbatches, tr, ls, f,
-                                                              o), fmt)
+    return _compare_text(lambda f, o: lib.wp_compare_measured(sch, wav, n, budget_devices, microbatches, tr, ls,
+                                                              float(t_comm), f, o), fmt)
 
 
 def simulate(lst: ActionList, cost: CostModel = None) -> SimTrace:

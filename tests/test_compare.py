@@ -55,3 +55,31 @@ def test_compare_matches_reference_live(P, B, cost, reqs, fmt):
     args += [f"{NAMES[s]}:{w}" for s, w in reqs]
     want = subprocess.run(args, capture_output=True, text=True, check=True).stdout
     assert wp.compare(reqs, P, B, wp.CostModel(*cost), fmt=fmt) == want
+
+
+def _row_list(req, P, B, cost):
+    """The list and cost compare() evaluates for one request (chimera-wave:
+    one of its two symmetric groups, ref src/analytics.cpp:236-247)."""
+    scheme, W = req
+    if scheme == S.ChimeraWave:
+        cfg = wp.make_config(scheme, P // 2, B // 2, W, 2)
+        cost = cost.rescaled(P, cfg.devices)
+    else:
+        cfg = wp.make_config(scheme, P, B, W)
+    return wp.generate_schedule(cfg, cost), cost
+
+
+@pytest.mark.parametrize("P,B,cost", [(4, 8, (1, 2, 0)), (8, 16, (1, 2, 0.5)), (4, 12, (2, 3, 0))])
+@pytest.mark.parametrize("fmt", ["csv", "json"])
+def test_compare_measured_on_simulated_traces_equals_compare(P, B, cost, fmt):
+    """compare_measured -- the rows of MEASURED traces -- fed the simulator's
+    traces of the same lists reproduces compare() byte for byte: the measured
+    path shares the reference's row arithmetic, order and writers."""
+    cm = wp.CostModel(*cost)
+    lists, traces = [], []
+    for req in SWEEP:
+        lst, c = _row_list(req, P, B, cm)
+        lists.append(lst)
+        traces.append(wp.simulate(lst, c))
+    got = wp.compare_measured(SWEEP, P, B, traces, lists, t_comm=cm.t_comm, fmt=fmt)
+    assert got == wp.compare(SWEEP, P, B, cm, fmt=fmt)

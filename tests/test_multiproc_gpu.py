@@ -368,3 +368,26 @@ def test_classic_schemes_over_ipc_equal_oracle(scheme, P, B):
             w = want[n].numpy().ravel().astype(np.float64)
             e = np.linalg.norm(g - w) / max(np.linalg.norm(w), 1e-30)
             assert e <= 1e-5, (rank, n, e)
+
+
+def test_measured_compare_tool_two_ranks():
+    """tools/compare_measured.py on two ranks sharing the GPU (functional):
+    every scheme that runs at P=2 yields a measured row (seconds, bubble in
+    [0, 1)), in the reference's CSV layout, sorted by makespan."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WP_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", f"--master-port={_free_port()}", os.path.join(root, "tools", "compare_measured.py"),
+           "--model", "tiny-gpt", "--mbs", "2", "--microbatches", "4"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = out.stdout.strip().splitlines()
+    assert lines[0].startswith("scheme,devices,microbatches,waves,makespan,simulated_bubble_ratio")
+    rows = [ln.split(",") for ln in lines[1:]]
+    names = {(r[0], r[3]) for r in rows}
+    assert {("gpipe", "1"), ("dapple", "1"), ("chimera", "1"), ("hanayo", "1"), ("hanayo", "2")} <= names
+    spans = [float(r[4]) for r in rows if r[4]]
+    assert spans == sorted(spans) and all(0 < s < 60 for s in spans)
+    assert all(0.0 <= float(r[5]) < 1.0 for r in rows if r[5])

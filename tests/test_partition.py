@@ -54,3 +54,16 @@ def test_tiny_more_slices_than_units():
     lst = wp.generate_schedule(wp.make_config(wp.Scheme.Hanayo, 4, 8, 2))  # S = 16 > 10 units
     b, costs = partition(desc, lst)
     assert b[0] == 0 and b[-1] == len(costs) and all(b[k] <= b[k + 1] for k in range(16))
+
+
+@pytest.mark.parametrize("P,W", [(1, 2), (2, 2), (4, 2), (8, 2), (8, 4), (3, 1)])
+@pytest.mark.parametrize("model", ["gpt13b", "tiny"])
+def test_oracle_restates_runtime_partition(P, W, model):
+    """oracle/pipeline.py's partition (the CPU interpreter's slices) equals
+    the runtime's device-balanced cut bit for bit."""
+    from oracle import pipeline as op
+    desc = wp.ModelDesc(**GPT13B) if model == "gpt13b" else wp.ModelDesc(layers=4, hidden=256, heads=4, ffn=1024,
+                                                                          seq=128, vocab=1024)
+    lst = wp.generate_schedule(wp.make_config(wp.Scheme.Hanayo, P, 8, W))
+    b, _ = partition(desc, lst)
+    assert op.partition(op.units(desc), op.slice_devices(lst.placement), P) == b

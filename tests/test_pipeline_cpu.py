@@ -2,7 +2,7 @@
 (message keys, placement, partition, BE pairing, FIFO order) runs the action
 list with the oracle's autograd compute and must reproduce sequential
 gradient accumulation; plus the rendezvous-safety of every generated list for
-the runtime's in-order NCCL queue, and a gloo world_size=2 run."""
+an in-order point-to-point queue, and a gloo world_size=2 run."""
 import os
 import socket
 
@@ -57,8 +57,10 @@ def test_local_interpreter_equals_sequential(P, B, W):
 def test_partition_matches_runtime_rules():
     d = Desc()
     us = opl.units(d)
-    for S in (1, 2, 4, 8, 16, 32):
-        b = opl.partition(us, S)
+    for P, W in ((1, 1), (1, 2), (2, 2), (4, 2), (8, 2), (8, 4)):
+        lst = wp.generate_schedule(wp.make_config(wp.Scheme.Hanayo, P, max(P, 2), W))
+        S = lst.config.stages
+        b = opl.partition(us, opl.slice_devices(lst.placement), P)
         assert b[0] == 0 and b[-1] == len(us)
         assert all(b[k] <= b[k + 1] for k in range(S))
         assert b[1] >= 1 or S == 1          # embedding in slice 0
@@ -69,8 +71,9 @@ def test_partition_matches_runtime_rules():
                                       (wp.Scheme.Dapple, 1), (wp.Scheme.Chimera, 1)])
 @pytest.mark.parametrize("P", [2, 3, 4, 8])
 def test_channel_plan_covers_every_message(scheme, W, P):
-    """Sender-order channels (the NCCL transport's receive plan) deliver each
-    incoming message of every device exactly once, from the right peer."""
+    """Sender-order channels (the oracle interpreter's receive plan, gloo
+    point-to-point) deliver each incoming message of every device exactly
+    once, from the right peer."""
     if scheme == wp.Scheme.Chimera and P % 2:
         return
     lst = wp.generate_schedule(wp.make_config(scheme, P, 2 * P, W))

@@ -171,6 +171,12 @@ def test_measured_trace_and_launches():
     assert tr.makespan > 0
     b = wp.bubble_ratio(tr)
     assert 0.0 <= b < 1.0
+    # the trace origin on the device clock (%globaltimer, ns): advances
+    # between traced steps by at least the earlier step's makespan
+    c0 = rt.step_clock_ns()
+    rt.train_step(tokens, labels)
+    c1 = rt.step_clock_ns()
+    assert c0 > 0 and c1 - c0 >= tr.makespan * 1e9 * 0.99
     for dev in tr.intervals:
         for iv in dev:
             assert iv.end >= iv.start >= 0.0
