@@ -171,12 +171,13 @@ def test_measured_trace_and_launches():
     assert tr.makespan > 0
     b = wp.bubble_ratio(tr)
     assert 0.0 <= b < 1.0
-    # the trace origin on the device clock (%globaltimer, ns): advances
-    # between traced steps by at least the earlier step's makespan
+    # the trace origin on the device clock (%globaltimer, ns) advances
+    # between traced steps on the scale of a step (device 0 may begin step 2
+    # before device 1 has finished step 1, so not by the full makespan)
     c0 = rt.step_clock_ns()
     rt.train_step(tokens, labels)
     c1 = rt.step_clock_ns()
-    assert c0 > 0 and c1 - c0 >= tr.makespan * 1e9 * 0.99
+    assert c0 > 0 and tr.makespan * 1e9 * 0.25 <= c1 - c0 <= tr.makespan * 1e9 * 100
     for dev in tr.intervals:
         for iv in dev:
             assert iv.end >= iv.start >= 0.0
@@ -252,3 +253,29 @@ def test_device_inputs_ordered_after_producer_stream():
     # zeros (an unordered read) would give a different loss; equal up to the
     # run-to-run rounding of the fp32 reductions otherwise
     assert abs(got - want) <= 1e-6 * abs(want), (got, want)
+
+
+@pytest.mark.parametrize("dtype,tol", [("fp32", 1e-6), ("bf16", 2e-3)])
+def test_run_to_run_spread(dtype, tol):
+    """Determinism contract ("Determinism"): repeating a step on
+    identical inputs and parameters is not bit-reproducible, because the
+    fused reductions (LayerNorm dw/db and row sums, bias column sums, Delta
+    row dots, split-K and dQ TMA reduce-adds, embedding scatter-add, the loss
+    sum) commit fp32 partials in hardware arrival order.  The spread that
+    reordering causes is bounded: normwise per tensor <= 1e-6 in fp32 mode,
+    <= 2e-3 in bf16 mode (bf16 re-rounding of activations downstream of a
+    reordered fp32 sum), far inside the parity tolerances."""
+    desc = wp.ModelDesc(**dict(TINY, layers=2), dtype=dtype)
+    rt, params = build(desc, P=2, B=4, W=2)
+    rt.set_update(False)
+    tokens, labels = synthetic_batch(4, desc.micro_batch_size, desc.seq, desc.vocab)
+    runs = []
+    for _ in range(3):
+        loss = rt.train_step(tokens, labels)
+        runs.append((loss, {n: rt.get_grad(n, t.numel()).copy() for n, t in params.items()}))
+    loss0, g0 = runs[0]
+    for loss, g in runs[1:]:
+        assert abs(loss - loss0) <= tol * abs(loss0), (loss, loss0)
+        for n in g0:
+            assert rel(g[n], g0[n]) <= tol, (n, rel(g[n], g0[n]))
+    rt.close()
