@@ -31,6 +31,7 @@
 #include <string>
 
 #include "kernels/attention.cuh"
+#include "kernels/softmax_math.cuh"
 #include "kernels/tc_common.cuh"
 
 namespace wpk {
@@ -50,6 +51,10 @@ __device__ unsigned long long g_bwt[16 * 32];
 namespace {
 
 using namespace tc;
+using namespace smx;
+
+// Of every 8 column pairs of a P^T row, this many take the FMA-pipe 2^x.
+constexpr int kBwPoly = 2;
 
 constexpr int T128 = 128;
 constexpr int ATOM = 128 * 64 * 2;  // SW128 atom: 128 rows x 64 bf16
@@ -99,11 +104,6 @@ struct BwParams {
   float* dbias;                 // [3h] fp32 QKV bias gradient (+=), or null
 };
 
-__device__ __forceinline__ float ex2f(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 __device__ __forceinline__ uint32_t swz(int r, int c) {  // 16-B chunk c of row r, SW128 K-major atoms
   const int atom = c >> 3, cc = c & 7;
@@ -136,7 +136,15 @@ __device__ __forceinline__ BwItem bw_item(const BwParams& p, int w) {
   return it;
 }
 
-// Persistent: one CTA per SM walks items w = blockIdx.x, + gridDim.x, ...
+// Item of this CTA's k-th round: the item list in snake order across the
+// CTAs (CTAs 0..G-1 on even rounds, G-1..0 on odd ones), which evens out the
+// per-CTA sums of the heaviest-first item sizes.
+__device__ __forceinline__ int bw_item_index(int k) {
+  const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  return k * G + ((k & 1) ? G - 1 - c : c);
+}
+
+// Persistent: one CTA per SM walks its items (bw_item_index(0), (1), ...)
 // Per-tile barriers run on the CTA's global tile counter g (across items),
 // per-item ones on its item counter, so the next item's K/V load, S^T and
 // dP^T overlap the previous item's dK / dV epilogue (done by the dQ drain
@@ -145,7 +153,8 @@ template <int D>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     flash_bwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                      const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
-                     const __grid_constant__ CUtensorMap map_dq, const __grid_constant__ BwParams p) {
+                     const __grid_constant__ CUtensorMap map_dq, const __grid_constant__ CUtensorMap map_dqkv,
+                     const __grid_constant__ BwParams p) {
   using Cfg = BwCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -173,7 +182,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   uint64_t* p_full = bars + 14;    // P^T of the tile written to TMEM (dV may start)
   uint64_t* lse_full = bars + 15;  // the tile's lse / Delta rows landed (bulk copies by warp 3)
   uint64_t* dl_full = bars + 16;
-  uint64_t* kv_empty = bars + 17;  // the item's last MMA read K / V
+  uint64_t* kv_empty = bars + 17;  // the item's last MMA read K (its last dQ)
+  uint64_t* v_empty = bars + 21;   // the item's last MMA read V (its last dP^T)
   uint64_t* dkv_free = bars + 18;  // the item's dK / dV read out of TMEM (epilogue)
   // The drain reads dQ in two D halves, each with its full / free barrier.
   uint64_t* dq_full_h[2] = {dq_full, bars + 19};
@@ -190,6 +200,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   if (warp == 1 && lane == 0) {
     mbar_init(kv_full, 1);
     mbar_init(kv_empty, 1);
+    mbar_init(v_empty, 1);
     for (int x = 0; x < 2; ++x) {
       mbar_init(&q_full[x], 1);
       mbar_init(&q_empty[x], 1);
@@ -225,7 +236,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     if (lane == 0) {
       int g = 0;  // global tile counter
       int ip = 0;
-      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ip) {
+      for (int w = bw_item_index(0); w < n_items; w = bw_item_index(ip + 1), ++ip) {
         const BwItem itm = bw_item(p, w);
         for (int t = 0; t < itm.n_it; ++t, ++g) {  // Q double-buffered (two tiles ahead), dO single
           const int qi = itm.i0 + t, x = g & 1;
@@ -240,12 +251,29 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           for (int a = 0; a < D / 64; ++a)
             tma_load_4d(&map_do, do_full, sDO + a * ATOM, a * 64, itm.head, qi * T128, itm.b);
           if (t == 0) {  // K / V after the first Q / dO: those buffers free up earlier
-            if (ip > 0) mbar_wait(kv_empty, (ip - 1) & 1);  // previous item's MMAs done with K / V
+            // V as soon as the previous item's last dP^T read it, K after its
+            // last dQ (the dV / dK MMAs of that tile still run)
             mbar_expect_tx(kv_full, 2 * Cfg::TILE);
+            if (ip > 0) mbar_wait(v_empty, (ip - 1) & 1);
 #pragma unroll
-            for (int a = 0; a < D / 64; ++a) {
-              tma_load_4d(&map_k, kv_full, sK + a * ATOM, a * 64, itm.head, itm.kj * T128, itm.b);
+            for (int a = 0; a < D / 64; ++a)
               tma_load_4d(&map_v, kv_full, sV + a * ATOM, a * 64, itm.head, itm.kj * T128, itm.b);
+            if (ip > 0) mbar_wait(kv_empty, (ip - 1) & 1);
+#pragma unroll
+            for (int a = 0; a < D / 64; ++a)
+              tma_load_4d(&map_k, kv_full, sK + a * ATOM, a * 64, itm.head, itm.kj * T128, itm.b);
+            // K / V are single-buffered: warm L2 with the next item's K / V
+            // and first Q / dO tiles now, so its loads at the item switch
+            // hit L2 instead of paying the DRAM latency.
+            if (w + static_cast<int>(gridDim.x) < n_items) {
+              const BwItem nx = bw_item(p, w + gridDim.x);
+#pragma unroll
+              for (int a = 0; a < D / 64; ++a) {
+                tma_prefetch_4d(&map_k, a * 64, nx.head, nx.kj * T128, nx.b);
+                tma_prefetch_4d(&map_v, a * 64, nx.head, nx.kj * T128, nx.b);
+                tma_prefetch_4d(&map_q, a * 64, nx.head, nx.i0 * T128, nx.b);
+                tma_prefetch_4d(&map_do, a * 64, nx.head, nx.i0 * T128, nx.b);
+              }
             }
           }
         }
@@ -258,7 +286,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       // (p_full), its Delta once they finished phase B (ds_full) -- each
       // lands while the other phase runs, off the softmax critical path.
       int g = 0;
-      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      for (int kk = 0, w = bw_item_index(0); w < n_items; w = bw_item_index(++kk)) {
         const BwItem itm = bw_item(p, w);
         for (int t = 0; t < itm.n_it; ++t, ++g) {
           const int64_t vec = (static_cast<int64_t>(itm.b) * p.heads + itm.head) * p.seq + (itm.i0 + t) * T128;
@@ -335,13 +363,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         tc_commit(do_empty);
       };
       int g = 0, ip = 0;
-      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ip) {
+      for (int w = bw_item_index(0); w < n_items; w = bw_item_index(ip + 1), ++ip) {
         const BwItem itm = bw_item(p, w);
         mbar_wait(kv_full, ip & 1);
         tc_fence_after();
         const int g0 = g;
         issue_s(g0);
         issue_dp(g0);
+        if (itm.n_it == 1) tc_commit(v_empty);  // the item's last dP^T: V may be reloaded
         if (ip > 0) mbar_wait(dkv_free, (ip - 1) & 1);  // previous item's dK / dV read out of TMEM
         issue_dv(g0, true);
         for (int t = 0; t < itm.n_it; ++t, ++g) {
@@ -364,6 +393,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 tc_mma(tmem + kColDP + 64 * h, desc_add(dDSm, k * 2048), desc_add(dKm, h * ATOM + k * 2048),
                        id_dq_half, k != 0);
               tc_commit(dq_full_h[h]);
+              BWT(14 + h, g);
             }
           } else {  // D = 64: one N=64 MMA; the drain still reads it in two halves
 #pragma unroll
@@ -372,6 +402,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             tc_commit(dq_full_h[0]);
             tc_commit(dq_full_h[1]);
           }
+          if (t + 1 == itm.n_it) tc_commit(kv_empty);  // the item's last dQ: K may be reloaded
           // dK += dS^T Q (reduction over the 128 queries)
 #pragma unroll
           for (int k = 0; k < T128 / 16; ++k) {
@@ -383,11 +414,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           BWT(2, g);
           if (t + 1 < itm.n_it) {
             issue_dp(g + 1);  // after the drain read dQ(g) out of TMEM
+            if (t + 2 == itm.n_it) tc_commit(v_empty);
             issue_dv(g + 1, false);
           }
         }
         tc_commit(dkv_done);
-        tc_commit(kv_empty);
       }
     }
   } else if (warp >= 4 && warp < 12) {
@@ -398,7 +429,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const int r = ew * 32 + lane;
     const uint32_t lb = static_cast<uint32_t>(ew * 32) << 16;
     int g = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    for (int kk = 0, w = bw_item_index(0); w < n_items; w = bw_item_index(++kk)) {
       const BwItem itm = bw_item(p, w);
       for (int t = 0; t < itm.n_it; ++t, ++g) {
         const float* lse = sLse;
@@ -417,10 +448,24 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           const int c0 = half * 64 + h2 * 32;
           float sv[32];
           tmem_ld32(tmem + lb + kColS + c0, sv);
+          const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int c = c0 + i;
-            pv[h2 * 32 + i] = (diag && c < r) ? 0.f : ex2f(sv[i] * p.scale_log2 - lse[c]);
+          for (int i = 0; i < 32; i += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(lse + c0 + i);  // broadcast
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              float2 e = ffma2(make_float2(sv[i + 2 * u], sv[i + 2 * u + 1]), sc2,
+                               u ? make_float2(-l4.z, -l4.w) : make_float2(-l4.x, -l4.y));
+              if ((((i >> 1) + u) & 7) < kBwPoly) {
+                e = ex2_poly2(e);
+              } else {
+                e.x = ex2(e.x);
+                e.y = ex2(e.y);
+              }
+              const int c = c0 + i + 2 * u;
+              pv[h2 * 32 + i + 2 * u] = (diag && c < r) ? 0.f : e.x;
+              pv[h2 * 32 + i + 2 * u + 1] = (diag && c + 1 < r) ? 0.f : e.y;
+            }
           }
           uint32_t pk[16];
 #pragma unroll
@@ -487,7 +532,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint8_t* slabs = sStage + ew * 2 * SLAB_BYTES;
     constexpr int NCH = D / 32, HALF = NCH / 2;
     int g = 0, ip = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ip) {
+    for (int w = bw_item_index(0); w < n_items; w = bw_item_index(ip + 1), ++ip) {
       const BwItem itm = bw_item(p, w);
       for (int t = 0; t < itm.n_it; ++t, ++g) {
         const int qi = itm.i0 + t;
@@ -497,6 +542,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           mbar_wait(dq_full_h[h], g & 1);
           tc_fence_after();
           if (h == 0 && warp == 12 && lane == 0) BWT(10, g);
+          if (h == 1 && warp == 12 && lane == 0) BWT(13, g);
           uint32_t u[HALF][32];
 #pragma unroll
           for (int c = 0; c < HALF; ++c) tmem_ld32_issue(tmem + lb + kColDP + (h * HALF + c) * 32, u[c]);
@@ -505,17 +551,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(dq_free_h[h]);  // these dQ columns read out: dP^T half h may start
           if (h == 1 && warp == 12 && lane == 0) BWT(11, g);
-          float v[HALF][32];
-#pragma unroll
-          for (int c = 0; c < HALF; ++c)
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[c][i] = __uint_as_float(u[c][i]);
 #pragma unroll
           for (int c = 0; c < HALF; ++c) {
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(u[c][i]);
             uint8_t* sb = slabs + ((h * HALF + c) & 1) * SLAB_BYTES;
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
-            slab_put_f32(sb, lane, v[c]);
+            slab_put_f32(sb, lane, v);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -525,42 +569,50 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           }
         }
       }
-      // dK, dV rows of this key tile -> dqkv.
+      // dK, dV rows of this key tile -> bf16 slabs (the drain's own, after
+      // their last reduce-add read them) -> TMA stores into dqkv, whole
+      // 128-byte row segments; the K / V bias-gradient column sums from the
+      // fp32 values.
       mbar_wait(dkv_done, ip & 1);
       tc_fence_after();
-      const int64_t row = static_cast<int64_t>(itm.b) * p.seq + itm.kj * T128 + ew * 32 + lane;
-      __nv_bfloat16* out = p.dqkv + row * 3 * p.hidden + itm.head * D;
+      const int row_k = itm.b * p.seq + itm.kj * T128 + ew * 32;
 #pragma unroll
       for (int part = 0; part < 2; ++part) {  // 0: dK, 1: dV
         const uint32_t col = part ? kColDV : Cfg::kColDK;
-        __nv_bfloat16* dst = out + (part ? 2 : 1) * p.hidden;
 #pragma unroll
-        for (int c = 0; c < D; c += 32) {
-          float v[32];
-          tmem_ld32(tmem + lb + col + c, v);
-#pragma unroll
-          for (int q = 0; q < 32; q += 8) {
-            uint4 u;
-            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(v[q + 2 * i], v[q + 2 * i + 1]);
-            *reinterpret_cast<uint4*>(dst + c + q) = u;
+        for (int hc = 0; hc < D / 64; ++hc) {
+          float v[64];
+          tmem_ld32(tmem + lb + col + hc * 64, v);
+          tmem_ld32(tmem + lb + col + hc * 64 + 32, v + 32);
+          uint8_t* sb = slabs + ((part * (D / 64) + hc) & 1) * SLAB_BYTES;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          slab_put_bf16(sb, lane, v);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_dqkv, sb, (part + 1) * p.hidden + itm.head * D + hc * 64, row_k);
+            bulk_commit();
           }
           if (p.dbias) {
             // bias gradient: column sums of this warp's 32 key rows (a
-            // transposing butterfly leaves column c + lane in v[0]), one
+            // transposing butterfly leaves column c + lane in w[0]), one
             // atomic per column per warp
 #pragma unroll
-            for (int sh = 16; sh >= 1; sh >>= 1) {
-              const bool up = (lane & sh) != 0;
+            for (int h2 = 0; h2 < 2; ++h2) {
+              float* w = v + 32 * h2;
 #pragma unroll
-              for (int i = 0; i < sh; ++i) {
-                const float send = up ? v[i] : v[i + sh];
-                const float keep = up ? v[i + sh] : v[i];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+              for (int sh = 16; sh >= 1; sh >>= 1) {
+                const bool up = (lane & sh) != 0;
+#pragma unroll
+                for (int i = 0; i < sh; ++i) {
+                  const float send = up ? w[i] : w[i + sh];
+                  const float keep = up ? w[i + sh] : w[i];
+                  w[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+                }
               }
+              atomicAdd(p.dbias + (part + 1) * p.hidden + itm.head * D + hc * 64 + 32 * h2 + lane, w[0]);
             }
-            atomicAdd(p.dbias + (part ? 2 : 1) * p.hidden + itm.head * D + c + lane, v[0]);
           }
         }
       }
@@ -701,7 +753,8 @@ void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const flo
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = std::min(p.n_tiles * s.heads * s.mbs, sms);  // persistent: one CTA per SM
   const CUtensorMap mdq = make_slab_map(dq_acc, kF32, s.hidden, int64_t(s.mbs) * s.seq, s.hidden);
-  k<<<grid, BW_THREADS, BwCfg<D>::SMEM, stream>>>(mq, mk, mv, mdo, mdq, p);
+  const CUtensorMap mdqkv = make_slab_map(dqkv, kBF16, 3LL * s.hidden, int64_t(s.mbs) * s.seq, 3LL * s.hidden);
+  k<<<grid, BW_THREADS, BwCfg<D>::SMEM, stream>>>(mq, mk, mv, mdo, mdq, mdqkv, p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("flash_attn_bwd: ") + cudaGetErrorString(e));
 }

@@ -21,7 +21,7 @@ for _ in range(3):
     lib.wp_debug_flash_bwd(mbs,seq,heads,d,causal,qkv.data_ptr(),ctx.data_ptr(),dout.data_ptr(),lse.data_ptr(),delta.data_ptr(),dq.data_ptr(),dqkv.data_ptr())
 buf=(C.c_ulonglong*512)()
 lib.wp_debug_bw_trace(buf,512)
-N={1:'mma_got_dS',2:'mma_dQ_committed',3:'mma_S_issued',12:'mma_dV_issue(p_full)',4:'mma_dP_issue(dqfree,dO)',5:'sm_got_S',6:'sm_phaseA_done',7:'sm_got_dP',8:'sm_got_pdsfree',9:'sm_dS_arrived',10:'dq_got',11:'dq_free_arrive'}
+N={13:'dq_got_h1',14:'mma_dQh0_issued',15:'mma_dQh1_issued',1:'mma_got_dS',2:'mma_dQ_committed',3:'mma_S_issued',12:'mma_dV_issue(p_full)',4:'mma_dP_issue(dqfree,dO)',5:'sm_got_S',6:'sm_phaseA_done',7:'sm_got_dP',8:'sm_got_pdsfree',9:'sm_dS_arrived',10:'dq_got',11:'dq_free_arrive'}
 ev=sorted((buf[e*32+j],e,j) for e in range(16) for j in range(32) if buf[e*32+j])
 t0=ev[0][0]
 for t,e,j in ev: print(f"{t-t0:8d} it={j:2d} {N.get(e,e)}")
