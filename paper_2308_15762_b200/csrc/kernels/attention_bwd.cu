@@ -4,8 +4,10 @@
 // memory while the query tiles i (causal: i >= j) stream through.  Per q tile:
 //   MMA        S^T  = K_j Q_i^T      (M=keys, N=queries, K=D)   -> TMEM
 //              dP^T = V_j dO_i^T     (M=keys, N=queries, K=D)   -> TMEM
-//   softmax    8 warps, one key row per thread, two query halves:
-//              P^T = 2^(s - lse2) -> bf16 back into TMEM (A of dV);
+//   softmax    16 warps, one key row per thread, four 32-query quarters
+//              (four warps per TMEM lane quadrant hide each other's TMEM
+//              and barrier latencies): P^T = 2^(s - lse2) -> bf16 back into
+//              the quarter's own S^T columns (A of dV);
 //              dS^T = P^T * (dP^T - Delta) / sqrt(D)  -> bf16 -> smem (SW128)
 //   MMA        dV_j += P^T dO_i (A from TMEM), dK_j += dS^T Q_i (accumulators
 //              in TMEM), dQ_i = dS K_j (A = the dS^T tile read MN-major)
@@ -17,8 +19,11 @@
 // dP^T(i+1) once the drain read dQ_i out of the shared columns, dV(i+1) as
 // soon as P^T(i+1) is in TMEM -- the next tile's softmax overlaps this
 // tile's dQ / dK and the drain.  Persistent CTAs (one per SM) walk the items
-// in a grouped, heaviest-first raster (see bw_item); lse / Delta of each
-// tile arrive by bulk copy off the softmax critical path.
+// in a grouped, heaviest-first raster (see bw_item), snake-ordered across
+// CTAs; V is reloaded for the next item after the last dP^T, K after the
+// last dQ; lse / Delta of each tile arrive by bulk copy off the softmax
+// critical path; dK / dV leave through the drain slabs by TMA stores.
+// 768 threads (80 registers each): every role works in 32-column pieces.
 // Delta = rowsum(dO * O) comes from the projection GEMM's epilogue (or
 // attn_bwd_prep); dq_finish converts the fp32 dQ accumulator to bf16 into dqkv.
 #include <cuda.h>
@@ -58,7 +63,8 @@ constexpr int kBwPoly = 2;
 
 constexpr int T128 = 128;
 constexpr int ATOM = 128 * 64 * 2;  // SW128 atom: 128 rows x 64 bf16
-constexpr int BW_THREADS = 512;     // warps 0-3 control, 4-11 softmax (two column halves), 12-15 dQ drain
+constexpr int SM_WARPS = 16;        // softmax warps: four per TMEM lane quadrant, 32 query columns each
+constexpr int BW_THREADS = 32 * (4 + SM_WARPS + 4);  // warps 0-3 control, 4-19 softmax, 20-23 dQ drain
 constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256;
 
 template <int D>
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     mbar_init(do_full, 1);
     mbar_init(do_empty, 1);
     mbar_init(s_full, 1);
-    mbar_init(ds_full, 8);
+    mbar_init(ds_full, SM_WARPS);
     mbar_init(pds_free, 1);  // dK and dQ MMAs done reading dS^T
     for (int h = 0; h < 2; ++h) {
       mbar_init(dq_full_h[h], 1);
@@ -217,7 +223,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     mbar_init(dkv_done, 1);
     mbar_init(dkv_free, 4);
     mbar_init(dp_full, 1);
-    mbar_init(p_full, 8);
+    mbar_init(p_full, SM_WARPS);
     mbar_init(lse_full, 1);
     mbar_init(dl_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -262,19 +268,6 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
             for (int a = 0; a < D / 64; ++a)
               tma_load_4d(&map_k, kv_full, sK + a * ATOM, a * 64, itm.head, itm.kj * T128, itm.b);
-            // K / V are single-buffered: warm L2 with the next item's K / V
-            // and first Q / dO tiles now, so its loads at the item switch
-            // hit L2 instead of paying the DRAM latency.
-            if (w + static_cast<int>(gridDim.x) < n_items) {
-              const BwItem nx = bw_item(p, w + gridDim.x);
-#pragma unroll
-              for (int a = 0; a < D / 64; ++a) {
-                tma_prefetch_4d(&map_k, a * 64, nx.head, nx.kj * T128, nx.b);
-                tma_prefetch_4d(&map_v, a * 64, nx.head, nx.kj * T128, nx.b);
-                tma_prefetch_4d(&map_q, a * 64, nx.head, nx.i0 * T128, nx.b);
-                tma_prefetch_4d(&map_do, a * 64, nx.head, nx.i0 * T128, nx.b);
-              }
-            }
           }
         }
       }
@@ -358,7 +351,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         BWT(12, g);
 #pragma unroll
         for (int k = 0; k < T128 / 16; ++k)
-          tc_mma_ts(tmem + kColDV, tmem + kColS + (k >> 2) * 64 + (k & 3) * 8, desc_add(dDOm, k * 2048), id_kv,
+          tc_mma_ts(tmem + kColDV, tmem + kColS + (k >> 1) * 32 + (k & 1) * 8, desc_add(dDOm, k * 2048), id_kv,
                     !(first && k == 0));
         tc_commit(do_empty);
       };
@@ -421,11 +414,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         tc_commit(dkv_done);
       }
     }
-  } else if (warp >= 4 && warp < 12) {
+  } else if (warp >= 4 && warp < 4 + SM_WARPS) {
     // -------------------------------------------------- P^T / dS^T (key rows)
-    // Two warps per TMEM lane quadrant: `half` picks query columns [64h, 64h+64).
+    // Four warps per TMEM lane quadrant: `grp` picks query columns
+    // [32 grp, 32 grp + 32); its packed P^T goes to S^T columns
+    // [32 grp, 32 grp + 16), inside the columns it alone reads.
     const int ew = warp & 3;
-    const int half = (warp - 4) >> 2;
+    const int grp = (warp - 4) >> 2;
+    const int c0 = grp * 32;
     const int r = ew * 32 + lane;
     const uint32_t lb = static_cast<uint32_t>(ew * 32) << 16;
     int g = 0;
@@ -440,43 +436,40 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         if (warp == 4 && lane == 0) BWT(5, g);
         const bool diag = p.causal && itm.i0 + t == itm.kj;
         // Phase A: P^T = 2^(s*scale - lse) from S^T alone; kept in registers
-        // for dS and written back over this half's S^T columns (bf16x2) as
+        // for dS and written back over this warp's S^T columns (bf16x2) as
         // the A operand of dV += P^T dO.
-        float pv[64];
+        float pv[32];
+        tmem_ld32(tmem + lb + kColS + c0, pv);
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int c0 = half * 64 + h2 * 32;
-          float sv[32];
-          tmem_ld32(tmem + lb + kColS + c0, sv);
-          const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        for (int i = 0; i < 32; i += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(lse + c0 + i);  // broadcast
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 l4 = *reinterpret_cast<const float4*>(lse + c0 + i);  // broadcast
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              float2 e = ffma2(make_float2(sv[i + 2 * u], sv[i + 2 * u + 1]), sc2,
-                               u ? make_float2(-l4.z, -l4.w) : make_float2(-l4.x, -l4.y));
-              if ((((i >> 1) + u) & 7) < kBwPoly) {
-                e = ex2_poly2(e);
-              } else {
-                e.x = ex2(e.x);
-                e.y = ex2(e.y);
-              }
-              const int c = c0 + i + 2 * u;
-              pv[h2 * 32 + i + 2 * u] = (diag && c < r) ? 0.f : e.x;
-              pv[h2 * 32 + i + 2 * u + 1] = (diag && c + 1 < r) ? 0.f : e.y;
+          for (int u = 0; u < 2; ++u) {
+            float2 e = ffma2(make_float2(pv[i + 2 * u], pv[i + 2 * u + 1]), sc2,
+                             u ? make_float2(-l4.z, -l4.w) : make_float2(-l4.x, -l4.y));
+            if ((((i >> 1) + u) & 7) < kBwPoly) {
+              e = ex2_poly2(e);
+            } else {
+              e.x = ex2(e.x);
+              e.y = ex2(e.y);
             }
+            const int c = c0 + i + 2 * u;
+            pv[i + 2 * u] = (diag && c < r) ? 0.f : e.x;
+            pv[i + 2 * u + 1] = (diag && c + 1 < r) ? 0.f : e.y;
           }
+        }
+        {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            __nv_bfloat162 hh = __floats2bfloat162_rn(pv[h2 * 32 + 2 * i], pv[h2 * 32 + 2 * i + 1]);
+            __nv_bfloat162 hh = __floats2bfloat162_rn(pv[2 * i], pv[2 * i + 1]);
             pk[i] = *reinterpret_cast<uint32_t*>(&hh);
           }
-          tmem_st16(tmem + lb + kColS + half * 64 + h2 * 16, pk);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) pv[h2 * 32 + i] *= p.scale;  // dS = (dP - Delta) * (P / sqrt(D))
+          tmem_st16(tmem + lb + kColS + c0, pk);
         }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pv[i] *= p.scale;  // dS = (dP - Delta) * (P / sqrt(D))
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
@@ -489,25 +482,24 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         if (warp == 4 && lane == 0) BWT(7, g);
         if (g > 0) mbar_wait(pds_free, (g - 1) & 1);  // dS^T buffer free (dK(g-1), dQ(g-1) read it)
         if (warp == 4 && lane == 0) BWT(8, g);
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int c0 = half * 64 + h2 * 32;
-          float dp[32], ds[32];
+        {
+          float dp[32];
           tmem_ld32(tmem + lb + kColDP + c0, dp);
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
             const float4 d4 = *reinterpret_cast<const float4*>(dl + c0 + i);
-            ds[i] = pv[h2 * 32 + i] * (dp[i] - d4.x);
-            ds[i + 1] = pv[h2 * 32 + i + 1] * (dp[i + 1] - d4.y);
-            ds[i + 2] = pv[h2 * 32 + i + 2] * (dp[i + 2] - d4.z);
-            ds[i + 3] = pv[h2 * 32 + i + 3] * (dp[i + 3] - d4.w);
+            const float2 a0 = fmul2(make_float2(pv[i], pv[i + 1]), fadd2(make_float2(dp[i], dp[i + 1]),
+                                                                         make_float2(-d4.x, -d4.y)));
+            const float2 a1 = fmul2(make_float2(pv[i + 2], pv[i + 3]), fadd2(make_float2(dp[i + 2], dp[i + 3]),
+                                                                             make_float2(-d4.z, -d4.w)));
+            dp[i] = a0.x, dp[i + 1] = a0.y, dp[i + 2] = a1.x, dp[i + 3] = a1.y;
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint4 ud;
             __nv_bfloat162* hd = reinterpret_cast<__nv_bfloat162*>(&ud);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) hd[i] = __floats2bfloat162_rn(ds[8 * q + 2 * i], ds[8 * q + 2 * i + 1]);
+            for (int i = 0; i < 4; ++i) hd[i] = __floats2bfloat162_rn(dp[8 * q + 2 * i], dp[8 * q + 2 * i + 1]);
             *reinterpret_cast<uint4*>(sDS + swz(r, c0 / 8 + q)) = ud;
           }
         }
@@ -518,7 +510,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         if (warp == 4 && lane == 0) BWT(9, g);
       }
     }
-  } else if (warp >= 12) {
+  } else if (warp >= 4 + SM_WARPS) {
     // ----------------------------- dQ drain (query rows) and dK / dV epilogue
     // TMEM -> fp32 SW128 slabs (two per warp, in their own buffer) -> TMA
     // bulk reduce-add into dq_acc: whole 128-byte row segments reduced in L2
@@ -541,21 +533,20 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         for (int h = 0; h < 2; ++h) {  // D half h of dQ (its own MMA commit)
           mbar_wait(dq_full_h[h], g & 1);
           tc_fence_after();
-          if (h == 0 && warp == 12 && lane == 0) BWT(10, g);
-          if (h == 1 && warp == 12 && lane == 0) BWT(13, g);
-          uint32_t u[HALF][32];
-#pragma unroll
-          for (int c = 0; c < HALF; ++c) tmem_ld32_issue(tmem + lb + kColDP + (h * HALF + c) * 32, u[c]);
-          tmem_wait_ld();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(dq_free_h[h]);  // these dQ columns read out: dP^T half h may start
-          if (h == 1 && warp == 12 && lane == 0) BWT(11, g);
+          if (h == 0 && warp == 4 + SM_WARPS && lane == 0) BWT(10, g);
+          if (h == 1 && warp == 4 + SM_WARPS && lane == 0) BWT(13, g);
+          // 32 columns at a time (registers: 768 threads leave ~80 each);
+          // the half's columns are free once its last chunk is in registers.
 #pragma unroll
           for (int c = 0; c < HALF; ++c) {
             float v[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(u[c][i]);
+            tmem_ld32(tmem + lb + kColDP + (h * HALF + c) * 32, v);
+            if (c == HALF - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(dq_free_h[h]);  // these dQ columns read out: dP^T half h may start
+              if (h == 1 && warp == 4 + SM_WARPS && lane == 0) BWT(11, g);
+            }
             uint8_t* sb = slabs + ((h * HALF + c) & 1) * SLAB_BYTES;
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
@@ -581,38 +572,43 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const uint32_t col = part ? kColDV : Cfg::kColDK;
 #pragma unroll
         for (int hc = 0; hc < D / 64; ++hc) {
-          float v[64];
-          tmem_ld32(tmem + lb + col + hc * 64, v);
-          tmem_ld32(tmem + lb + col + hc * 64 + 32, v + 32);
           uint8_t* sb = slabs + ((part * (D / 64) + hc) & 1) * SLAB_BYTES;
           if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
-          slab_put_bf16(sb, lane, v);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&map_dqkv, sb, (part + 1) * p.hidden + itm.head * D + hc * 64, row_k);
-            bulk_commit();
-          }
-          if (p.dbias) {
-            // bias gradient: column sums of this warp's 32 key rows (a
-            // transposing butterfly leaves column c + lane in w[0]), one
-            // atomic per column per warp
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              float* w = v + 32 * h2;
+          for (int h2 = 0; h2 < 2; ++h2) {  // 32 columns at a time
+            float v[32];
+            tmem_ld32(tmem + lb + col + hc * 64 + 32 * h2, v);
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              uint4 u;
+              __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) hh[i] = __floats2bfloat162_rn(v[8 * cc + 2 * i], v[8 * cc + 2 * i + 1]);
+              *reinterpret_cast<uint4*>(sb + slab_off(lane, 4 * h2 + cc)) = u;
+            }
+            if (p.dbias) {
+              // bias gradient: column sums of this warp's 32 key rows (a
+              // transposing butterfly leaves column c + lane in v[0]), one
+              // atomic per column per warp
 #pragma unroll
               for (int sh = 16; sh >= 1; sh >>= 1) {
                 const bool up = (lane & sh) != 0;
 #pragma unroll
                 for (int i = 0; i < sh; ++i) {
-                  const float send = up ? w[i] : w[i + sh];
-                  const float keep = up ? w[i + sh] : w[i];
-                  w[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+                  const float send = up ? v[i] : v[i + sh];
+                  const float keep = up ? v[i + sh] : v[i];
+                  v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
                 }
               }
-              atomicAdd(p.dbias + (part + 1) * p.hidden + itm.head * D + hc * 64 + 32 * h2 + lane, w[0]);
+              atomicAdd(p.dbias + (part + 1) * p.hidden + itm.head * D + hc * 64 + 32 * h2 + lane, v[0]);
             }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_dqkv, sb, (part + 1) * p.hidden + itm.head * D + hc * 64, row_k);
+            bulk_commit();
           }
         }
       }

@@ -19,9 +19,11 @@ b = torch.randn(N, K, device="cuda", dtype=torch.bfloat16)
 c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
 aux = torch.empty(M, N, device="cuda", dtype=torch.bfloat16) if gelu else None
 bias = torch.zeros(N, device="cuda") if gelu else None
+lib.wp_last_error.restype = C.c_char_p
 for _ in range(2):
-    lib.wp_debug_gemm(M, N, K, 1, 1, 1, a.data_ptr(), K, 0, 0, 0, b.data_ptr(), K, 0, 0, 0, 3 if gelu else 0, 1.0,
+    st = lib.wp_debug_gemm(M, N, K, 1, 1, 1, a.data_ptr(), K, 0, 0, 0, b.data_ptr(), K, 0, 0, 0, 3 if gelu else 0, 1.0,
                       c.data_ptr(), 1, N, 0, 0, bias.data_ptr() if gelu else None, None,
                       aux.data_ptr() if gelu else None)
+    assert st == 0, lib.wp_last_error().decode()
     torch.matmul(a, b.t())
 torch.cuda.synchronize()
