@@ -9,7 +9,7 @@ lib=_native.lib
 lib.wp_debug_flash_fwd.argtypes=[C.c_int]*5+[C.c_void_p]*3
 lib.wp_debug_flash_bwd.argtypes=[C.c_int]*5+[C.c_void_p]*7
 lib.wp_debug_bw_trace.argtypes=[C.c_void_p, C.c_int]
-mbs,seq,heads,d=16,1024,16,128
+mbs,seq,heads,d=16,1024,16,int(os.environ.get('D','128'))
 causal=int(os.environ.get('CAUSAL','0'))
 h=heads*d
 qkv=torch.randn(mbs*seq,3*h,device='cuda').bfloat16()

@@ -14,7 +14,7 @@ lib.wp_debug_flash_fwd.argtypes = [C.c_int] * 5 + [C.c_void_p] * 3
 lib.wp_debug_fa_trace.argtypes = [C.c_void_p, C.c_int]
 NAMES = {1: "S_commit", 2: "PV_commit", 3: "sm_wait_S", 4: "sm_got_S", 5: "sm_wait_O", 6: "sm_got_O",
          7: "sm_P_ready", 8: "mma_enter_S", 9: "mma_enter_PV", 10: "mma_issue_S", 11: "mma_issue_PV"}
-mbs, seq, heads, d = 8, 1024, 16, 128
+mbs, seq, heads, d = 8, 1024, 16, int(os.environ.get("D", "128"))
 causal = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 h = heads * d
 qkv = torch.randn(mbs * seq, 3 * h, device="cuda").bfloat16()
