@@ -102,6 +102,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
 struct BwParams {
   int batch, seq, heads, n_tiles, causal, hidden;
   int group;  // (batch, head) pairs per raster group (0: all)
+  int dq_halves;  // D = 128: dQ as two N = 64 MMA groups (A/B switch)
   float scale_log2, scale;
   const float* lse2;
   const float* delta;
@@ -378,7 +379,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
           // into the dP^T columns, first and in two D halves with their own
           // commits, so the drain of the first half starts while the second
           // half and dK run.
-          if constexpr (D == 128) {
+          // (Two N = 64 halves with their own commits let the drain start
+          // earlier but double the MMA instructions, each of which costs
+          // about as much at N = 64 as at N = 128: one N = D group by
+          // default, halves with WP_BW_DQ_HALVES=1.)
+          if (D == 128 && p.dq_halves) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -388,7 +393,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
               tc_commit(dq_full_h[h]);
               BWT(14 + h, g);
             }
-          } else {  // D = 64: one N=64 MMA; the drain still reads it in two halves
+          } else {  // one N = D group; the drain still reads it in two halves
 #pragma unroll
             for (int k = 0; k < T128 / 16; ++k)
               tc_mma(tmem + kColDP, desc_add(dDSm, k * 2048), desc_add(dKm, k * 2048), id_dq, k != 0);
@@ -745,6 +750,8 @@ void launch_bwd(const AttnShape& s, const void* qkv, const void* dout, const flo
     return g ? std::atoi(g) : 32;
   }();
   p.group = group;
+  static const int dq_halves = std::getenv("WP_BW_DQ_HALVES") ? std::atoi(std::getenv("WP_BW_DQ_HALVES")) : 0;
+  p.dq_halves = dq_halves;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = std::min(p.n_tiles * s.heads * s.mbs, sms);  // persistent: one CTA per SM
