@@ -252,6 +252,20 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
           for (int a = 0; a < D / 64; ++a)
             tma_load_4d(&map_q, &q_full[x], sQ + x * Cfg::TILE + a * ATOM, a * 64, itm.head, qi * T128, itm.b);
+          // Two tiles before this item ends, warm L2 with the next item's
+          // K / V (single-buffered in shared memory, they are loaded only
+          // once this item's last dP^T / dQ read the current ones).
+          if (t == max(0, itm.n_it - 2)) {
+            const int wn = bw_item_index(ip + 1);
+            if (wn < n_items) {
+              const BwItem nx = bw_item(p, wn);
+#pragma unroll
+              for (int a = 0; a < D / 64; ++a) {
+                tma_prefetch_4d(&map_k, a * 64, nx.head, nx.kj * T128, nx.b);
+                tma_prefetch_4d(&map_v, a * 64, nx.head, nx.kj * T128, nx.b);
+              }
+            }
+          }
           if (g >= 1) mbar_wait(do_empty, (g - 1) & 1);  // dV(g-1) read dO(g-1)
           mbar_expect_tx(do_full, Cfg::TILE);
 #pragma unroll
