@@ -44,6 +44,7 @@ namespace wpk {
 // Debug timeline of CTA 0 (build with -DWP_BW_TRACE; tools/bw_trace_probe.py):
 // clock64 per (event, global tile g < 32).
 __device__ unsigned long long g_bwt[16 * 32];
+__device__ unsigned long long g_bw_cta[2 * 160];  // per-CTA start / end (%globaltimer)
 #define BWT(ev, j)                                                        \
   do {                                                                    \
     if (blockIdx.x == 0 && (j) < 32) g_bwt[(ev) * 32 + (j)] = clock64(); \
@@ -238,6 +239,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#ifdef WP_BW_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 160) g_bw_cta[2 * blockIdx.x] = global_ns();
+#endif
 
   if (warp == 0) {
     if (lane == 0) {
@@ -641,6 +645,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
   tc_fence_before();
   __syncwarp();
   __syncthreads();
+#ifdef WP_BW_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 160) g_bw_cta[2 * blockIdx.x + 1] = global_ns();
+#endif
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -805,6 +812,7 @@ int flash_attn_bwd(const AttnShape& s, const void* qkv, const void* out, const v
 #ifdef WP_BW_TRACE
 extern "C" int wp_debug_bw_trace(unsigned long long* out, int n) {
   cudaDeviceSynchronize();
+  if (n > 512) cudaMemcpyFromSymbol(out + 512, wpk::g_bw_cta, sizeof(unsigned long long) * (n - 512 < 320 ? n - 512 : 320));
   return cudaMemcpyFromSymbol(out, wpk::g_bwt, sizeof(unsigned long long) * (n < 512 ? n : 512)) == cudaSuccess ? 0 : 1;
 }
 #endif

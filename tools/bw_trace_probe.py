@@ -19,9 +19,14 @@ dq=torch.empty(mbs*seq,h,device='cuda'); dqkv=torch.empty(mbs*seq,3*h,device='cu
 lib.wp_debug_flash_fwd(mbs,seq,heads,d,causal,qkv.data_ptr(),ctx.data_ptr(),lse.data_ptr())
 for _ in range(3):
     lib.wp_debug_flash_bwd(mbs,seq,heads,d,causal,qkv.data_ptr(),ctx.data_ptr(),dout.data_ptr(),lse.data_ptr(),delta.data_ptr(),dq.data_ptr(),dqkv.data_ptr())
-buf=(C.c_ulonglong*512)()
-lib.wp_debug_bw_trace(buf,512)
+buf=(C.c_ulonglong*832)()
+lib.wp_debug_bw_trace(buf,832)
 N={13:'dq_got_h1',14:'mma_dQh0_issued',15:'mma_dQh1_issued',1:'mma_got_dS',2:'mma_dQ_committed',3:'mma_S_issued',12:'mma_dV_issue(p_full)',4:'mma_dP_issue(dqfree,dO)',5:'sm_got_S',6:'sm_phaseA_done',7:'sm_got_dP',8:'sm_got_pdsfree',9:'sm_dS_arrived',10:'dq_got',11:'dq_free_arrive'}
 ev=sorted((buf[e*32+j],e,j) for e in range(16) for j in range(32) if buf[e*32+j])
 t0=ev[0][0]
 for t,e,j in ev: print(f"{t-t0:8d} it={j:2d} {N.get(e,e)}")
+cta=[(buf[512+2*i],buf[513+2*i]) for i in range(148) if buf[512+2*i]]
+if cta:
+    t0=min(a for a,b in cta); durs=sorted(b-a for a,b in cta); ends=sorted(b-t0 for a,b in cta)
+    print(f"CTAs {len(cta)}: duration min {durs[0]/1e3:.1f} us  median {durs[len(durs)//2]/1e3:.1f}  max {durs[-1]/1e3:.1f}; "
+          f"end spread {ends[0]/1e3:.1f}..{ends[-1]/1e3:.1f} us; starts spread {(max(a for a,b in cta)-t0)/1e3:.1f} us")
