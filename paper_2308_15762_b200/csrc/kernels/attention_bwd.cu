@@ -76,6 +76,11 @@ struct BwCfg {
   // K, V, Q[2], dO, dS^T, drain slabs, lse/delta (single-buffered), barriers
   static constexpr int SMEM = 5 * TILE + PT + STAGE + 2 * T128 * 4 + 1024 + 256;  // 16 barriers + TMEM slot
   static constexpr uint32_t kColDK = kColDV + D;
+  // dQ: at D = 64 the accumulators leave 128 columns free, so dQ gets its
+  // own (dP^T(next) need not wait for the drain); at D = 128 it reuses the
+  // dP^T columns.
+  static constexpr bool DQ_OWN = D == 64;
+  static constexpr uint32_t kColDQ = DQ_OWN ? kColDK + D : kColDP;
 };
 
 // dV += P^T dO with P^T read from tensor memory (kind::f16, A in TMEM: lane =
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
       // (both halves) out of them.
       auto issue_dp = [&](int g) {
         mbar_wait(do_full, g & 1);
-        if (g > 0) {
+        if (g > 0 && !Cfg::DQ_OWN) {
           mbar_wait(dq_free_h[0], (g - 1) & 1);
           mbar_wait(dq_free_h[1], (g - 1) & 1);
         }
@@ -412,9 +417,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
               BWT(14 + h, g);
             }
           } else {  // one N = D group; the drain still reads it in two halves
+            if (Cfg::DQ_OWN && g > 0) {  // own columns: the drain must have read dQ(g-1)
+              mbar_wait(dq_free_h[0], (g - 1) & 1);
+              mbar_wait(dq_free_h[1], (g - 1) & 1);
+              tc_fence_after();
+            }
 #pragma unroll
             for (int k = 0; k < T128 / 16; ++k)
-              tc_mma(tmem + kColDP, desc_add(dDSm, k * 2048), desc_add(dKm, k * 2048), id_dq, k != 0);
+              tc_mma(tmem + Cfg::kColDQ, desc_add(dDSm, k * 2048), desc_add(dKm, k * 2048), id_dq, k != 0);
             tc_commit(dq_full_h[0]);
             tc_commit(dq_full_h[1]);
           }
@@ -563,7 +573,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
           for (int c = 0; c < HALF; ++c) {
             float v[32];
-            tmem_ld32(tmem + lb + kColDP + (h * HALF + c) * 32, v);
+            tmem_ld32(tmem + lb + Cfg::kColDQ + (h * HALF + c) * 32, v);
             if (c == HALF - 1) {
               tc_fence_before();
               __syncwarp();
