@@ -79,16 +79,27 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
   float v[CPC];
   tmem_ld32(taddr, v);
   if constexpr (CPC == 64) tmem_ld32(taddr + 32, v + 32);
+  // alpha / bias with packed f32x2 arithmetic (the epilogue warps share
+  // their sub-partitions with the MMA issuer: fewer issue slots here keep
+  // the tensor pipe fed); no work at all for alpha = 1 without a bias.
+  const float2 al2 = make_float2(e.alpha, e.alpha);
   if (bias && gcol + CPC <= p.N) {
 #pragma unroll
     for (int i = 0; i < CPC; i += 4) {
       const float4 b4 = *reinterpret_cast<const float4*>(bias + gcol + i);
-      v[i] = fmaf(v[i], e.alpha, b4.x), v[i + 1] = fmaf(v[i + 1], e.alpha, b4.y);
-      v[i + 2] = fmaf(v[i + 2], e.alpha, b4.z), v[i + 3] = fmaf(v[i + 3], e.alpha, b4.w);
+      const float2 r0 = smx::ffma2(make_float2(v[i], v[i + 1]), al2, make_float2(b4.x, b4.y));
+      const float2 r1 = smx::ffma2(make_float2(v[i + 2], v[i + 3]), al2, make_float2(b4.z, b4.w));
+      v[i] = r0.x, v[i + 1] = r0.y, v[i + 2] = r1.x, v[i + 3] = r1.y;
     }
-  } else {
+  } else if (bias) {
 #pragma unroll
-    for (int i = 0; i < CPC; ++i) v[i] = v[i] * e.alpha + ((bias && gcol + i < p.N) ? bias[gcol + i] : 0.f);
+    for (int i = 0; i < CPC; ++i) v[i] = v[i] * e.alpha + (gcol + i < p.N ? bias[gcol + i] : 0.f);
+  } else if (e.alpha != 1.f) {
+#pragma unroll
+    for (int i = 0; i < CPC; i += 2) {
+      const float2 r = smx::fmul2(make_float2(v[i], v[i + 1]), al2);
+      v[i] = r.x, v[i + 1] = r.y;
+    }
   }
   if (needs_in) {
     mbar_wait(&sbar[buf], (sphase >> buf) & 1);
@@ -105,10 +116,17 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
     }
     if (mode == kEpiResidual) {
 #pragma unroll
-      for (int i = 0; i < CPC; ++i) v[i] += x[i];
+      for (int i = 0; i < CPC; i += 2) {
+        const float2 r = smx::fadd2(make_float2(v[i], v[i + 1]), make_float2(x[i], x[i + 1]));
+        v[i] = r.x, v[i + 1] = r.y;
+      }
     } else {
 #pragma unroll
-      for (int i = 0; i < CPC; ++i) v[i] *= gelu_grad_fast(x[i]);
+      for (int i = 0; i < CPC; i += 2) {
+        const float2 gg = gelu_grad_fast2(make_float2(x[i], x[i + 1]));
+        const float2 r = smx::fmul2(make_float2(v[i], v[i + 1]), gg);
+        v[i] = r.x, v[i + 1] = r.y;
+      }
     }
   }
   auto put = [&](uint8_t* slab) {
@@ -121,7 +139,10 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
     for (int i = 0; i < CPC; ++i) v[i] = round_to(dt, v[i]);  // GELU of the stored pre-activation
     put(sb);
 #pragma unroll
-    for (int i = 0; i < CPC; ++i) v[i] = gelu_fast(v[i]);
+    for (int i = 0; i < CPC; i += 2) {
+      const float2 r = gelu_fast2(make_float2(v[i], v[i + 1]));
+      v[i] = r.x, v[i + 1] = r.y;
+    }
     put(sg);
     fence_proxy_async_smem();
     __syncwarp();

@@ -3,6 +3,8 @@
 // descriptor, tile decoding and the fused epilogue.
 #pragma once
 
+#include "kernels/softmax_math.cuh"
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -272,6 +274,30 @@ __device__ __forceinline__ float gelu_grad_fast(float x) {
   const float x2 = x * x;
   const float t = tanh_fast(k0 * fmaf(k1 * x, x2, x));
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * fmaf(3.0f * k1, x2, 1.0f);
+}
+
+// The same two on a pair of columns with packed f32x2 arithmetic (FFMA2 /
+// FMUL2 / FADD2: half the FP32 issue slots of the scalar forms, which share
+// the SM sub-partition with the MMA issuer in the GEMM epilogue).
+__device__ __forceinline__ float2 gelu_fast2(float2 x) {
+  using namespace smx;
+  const float2 k0 = make_float2(0.7978845608028654f, 0.7978845608028654f), k1 = make_float2(0.044715f, 0.044715f);
+  const float2 c = ffma2(fmul2(k1, x), fmul2(x, x), x);
+  const float2 d = fmul2(k0, c);
+  const float2 t = make_float2(tanh_fast(d.x), tanh_fast(d.y));
+  return fmul2(fmul2(make_float2(0.5f, 0.5f), x), fadd2(make_float2(1.0f, 1.0f), t));
+}
+__device__ __forceinline__ float2 gelu_grad_fast2(float2 x) {
+  using namespace smx;
+  const float2 k0 = make_float2(0.7978845608028654f, 0.7978845608028654f), k1 = make_float2(0.044715f, 0.044715f);
+  const float2 one = make_float2(1.0f, 1.0f), half = make_float2(0.5f, 0.5f);
+  const float2 x2 = fmul2(x, x);
+  const float2 d = fmul2(k0, ffma2(fmul2(k1, x), x2, x));
+  const float2 t = make_float2(tanh_fast(d.x), tanh_fast(d.y));
+  const float2 omt2 = ffma2(make_float2(-t.x, -t.y), t, one);                       // 1 - t^2
+  const float2 s = ffma2(make_float2(3.0f * 0.044715f, 3.0f * 0.044715f), x2, one);  // 1 + 3 k1 x^2
+  const float2 q = fmul2(fmul2(fmul2(fmul2(half, x), omt2), k0), s);
+  return ffma2(half, fadd2(one, t), q);
 }
 
 __device__ __forceinline__ float round_to(int dtype, float x) {
