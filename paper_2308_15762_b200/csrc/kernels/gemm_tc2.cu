@@ -135,9 +135,23 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
   };
   if (mode == kEpiGelu) {
     uint8_t* sg = slabs + (buf ^ 1) * SLAB_BYTES;
+    // GELU of the stored (bf16-rounded) pre-activation: round once, packed,
+    // and store the packed words as they are.
+    if constexpr (CPC == 64) {
+      uint32_t pk[CPC / 2];
 #pragma unroll
-    for (int i = 0; i < CPC; ++i) v[i] = round_to(dt, v[i]);  // GELU of the stored pre-activation
-    put(sb);
+      for (int i = 0; i < CPC; i += 2) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(v[i], v[i + 1]);
+        pk[i / 2] = *reinterpret_cast<const uint32_t*>(&h);
+        const float2 f = __bfloat1622float2(h);
+        v[i] = f.x, v[i + 1] = f.y;
+      }
+      slab_put_bf16_packed(sb, lane, pk);
+    } else {
+#pragma unroll
+      for (int i = 0; i < CPC; ++i) v[i] = round_to(dt, v[i]);
+      put(sb);
+    }
 #pragma unroll
     for (int i = 0; i < CPC; i += 2) {
       const float2 r = gelu_fast2(make_float2(v[i], v[i + 1]));
@@ -211,14 +225,37 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
     slab_get_bf16(sx, lane, xv);
     const int row = row0 + lane;
     if (row < p.M && gcol < p.N) {
-      float acc = 0.f;
+      // dot of the bf16-rounded row with x: packed rounding and FFMA2 into
+      // two independent pair accumulators
+      float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-      for (int i = 0; i < CPC; ++i) acc += round_to(kBF16, v[i]) * xv[i];
+      for (int i = 0; i < CPC; i += 2) {
+        const float2 rv = __bfloat1622float2(__floats2bfloat162_rn(v[i], v[i + 1]));
+        acc2[(i >> 1) & 1] = smx::ffma2(rv, make_float2(xv[i], xv[i + 1]), acc2[(i >> 1) & 1]);
+      }
+      const float acc = (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
       const int64_t ngrp = p.N / e.rd_group;
       atomicAdd(e.rd_out + (row / e.rd_seq * ngrp + gcol / e.rd_group) * e.rd_seq + row % e.rd_seq, acc);
     }
   }
-  if (e.colsum) {
+  if (e.colsum && CPC == 64 && mode != kEpiGelu) {
+    // Column sums of the bf16 C just staged (the stored values, which are
+    // what the next GEMMs and the reference's rounding points see): lane l
+    // reads columns 2l, 2l+1 down the slab's 32 rows (one 128-byte row per
+    // warp load, conflict-free) -- half the instructions of the butterfly
+    // below; rows past M skipped.
+    __syncwarp();
+    const int rows = min(32, p.M - row0);
+    float2 cs = make_float2(0.f, 0.f);
+#pragma unroll 8
+    for (int r = 0; r < rows; ++r) {
+      const uint32_t u = *reinterpret_cast<const uint32_t*>(sb + slab_off(r, lane >> 2) + (lane & 3) * 4);
+      cs = smx::fadd2(cs, __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u)));
+    }
+    const int col = gcol + 2 * lane;
+    if (col < p.N) atomicAdd(e.colsum + col, cs.x);
+    if (col + 1 < p.N) atomicAdd(e.colsum + col + 1, cs.y);
+  } else if (e.colsum) {
     // Column sums of this slab's 32 rows (one per lane): a transposing
     // butterfly leaves column (32q + lane) in v[32q] after 31 shuffles per 32
     // columns, then one atomic per column per warp (rows past M masked).

@@ -480,6 +480,12 @@ __device__ __forceinline__ void slab_put_bf16(uint8_t* slab, int r, const float*
     *reinterpret_cast<uint4*>(slab + slab_off(r, c)) = u;
   }
 }
+// Same with the row already packed as bf16x2 (32 words).
+__device__ __forceinline__ void slab_put_bf16_packed(uint8_t* slab, int r, const uint32_t* pk /*32*/) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<uint4*>(slab + slab_off(r, c)) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+}
 __device__ __forceinline__ void slab_get_bf16(const uint8_t* slab, int r, float* v /*64*/) {
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
