@@ -180,6 +180,34 @@ def cpu_port_sample(desc, threads=None):
                                         causal=desc.causal)), dt, threads
 
 
+# Full-step CPU path when the whole step is small enough to time directly
+# (C1 on the full action list; larger models extrapolate).
+FULL_LIST_TFLOP = 2.0
+
+
+def cpu_full_list_step(args, P, threads=None):
+    """Time the oracle's torch-CPU fp32 interpreter of the whole Hanayo action
+    list (the reference's generator restated in oracle/schedule.py, pinned to
+    its goldens) over B microbatches; returns (samples/s, seconds, threads)."""
+    import torch
+    from oracle import model as om
+    from oracle import pipeline as opl
+    from oracle import schedule as osch
+    from oracle.data import synthetic_batch
+    threads = threads or os.cpu_count()
+    torch.set_num_threads(threads)
+    desc = Workload(args)
+    cfg = osch.make_config(osch.HANAYO, P, args.microbatches, args.waves)
+    acts, pl = osch.generate_schedule(cfg)
+    placement = [[sl[0] for sl in row] for row in pl]
+    params = {k: v.float() for k, v in om.init_params(desc, seed=1).items()}
+    tokens, labels = synthetic_batch(args.microbatches, args.mbs, desc.seq, desc.vocab)
+    t0 = time.perf_counter()
+    opl.run_local(desc, params, acts, placement, args.microbatches, tokens, labels, dtype=torch.float32)
+    dt = time.perf_counter() - t0
+    return args.microbatches * args.mbs / dt, dt, threads
+
+
 def ref_schedule_time(P, B, W):
     """The reference's own CPU path (oracle/_ref: its src/*.cpp, generate +
     simulate), single-threaded as the reference is."""
@@ -200,21 +228,27 @@ def run_reference(args, rank, world):
         return
     desc = Workload(args)
     P = args.gpus
+    full = desc.flops_per_sample() * args.microbatches * args.mbs <= FULL_LIST_TFLOP * 1e12
+    sample_fn = (lambda: cpu_full_list_step(args, P)) if full else (lambda: cpu_port_sample(Workload(args)))
     for _ in range(args.warmup):
-        cpu_port_sample(desc)
+        sample_fn()
     vals, per = [], []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, dt, cores = cpu_port_sample(Workload(args))
+        v, dt, cores = sample_fn()
         vals.append(v)
         per.append(dt)
     wall = time.perf_counter() - t0
     value = statistics.median(vals)
     ref_ms = ref_schedule_time(P, args.microbatches, args.waves)
-    sample = (f"1 sequence x (embedding + 1 of {desc.layers} layers + LM head) of {args.model}, fp32 torch CPU "
-              f"fwd+bwd ({statistics.median(per):.2f} s), extrapolated to the full model by FLOPs; "
-              f"schedule generate+simulate by the reference's own code (oracle/_ref): "
-              f"{ref_ms if ref_ms is not None else 'n/a'} ms")
+    sched = (f"schedule generate+simulate by the reference's own code (oracle/_ref): "
+             f"{ref_ms if ref_ms is not None else 'n/a'} ms")
+    if full:
+        sample = (f"the whole Hanayo P={P} W={args.waves} B={args.microbatches} action list of {args.model} "
+                  f"(mbs {args.mbs}), fp32 torch CPU interpreter ({statistics.median(per):.2f} s per step); {sched}")
+    else:
+        sample = (f"1 sequence x (embedding + 1 of {desc.layers} layers + LM head) of {args.model}, fp32 torch CPU "
+                  f"fwd+bwd ({statistics.median(per):.2f} s), extrapolated to the full model by FLOPs; {sched}")
     line = {
         "impl": "reference", "metric": "samples/sec (Hanayo W=2 train step)", "value": value,
         "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -474,10 +508,15 @@ def main():
     flops_step = flops_per_sample(MODELS[args.model]) * args.microbatches * args.mbs * D
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, dt, cores = cpu_port_sample(desc)
-        cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
-               "sample": f"1 sequence x (embedding + 1 of {desc.layers} layers + LM head), fp32 torch CPU fwd+bwd "
-                         f"({dt:.2f} s), extrapolated to the {desc.layers}-layer model by FLOPs"}
+        if flops_step <= FULL_LIST_TFLOP * 1e12:
+            v, dt, cores = cpu_full_list_step(args, 1)
+            smp = (f"the whole Hanayo P=1 W={args.waves} B={args.microbatches} action list, fp32 torch CPU "
+                   f"interpreter ({dt:.2f} s per step)")
+        else:
+            v, dt, cores = cpu_port_sample(desc)
+            smp = (f"1 sequence x (embedding + 1 of {desc.layers} layers + LM head), fp32 torch CPU fwd+bwd "
+                   f"({dt:.2f} s), extrapolated to the {desc.layers}-layer model by FLOPs")
+        cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": smp}
     line = {
         "metric": "samples/sec (Hanayo W=2 train step)", "value": value, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,

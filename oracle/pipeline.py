@@ -148,9 +148,9 @@ def incoming(per_device, d):
 class Device:
     """One pipeline device's parameters and program state."""
 
-    def __init__(self, desc, params, slices, bounds, us):
+    def __init__(self, desc, params, slices, bounds, us, dtype=torch.float64):
         self.desc, self.bounds, self.us = desc, bounds, us
-        self.P = {k: v.detach().clone().double().requires_grad_(True) for k, v in params.items()}
+        self.P = {k: v.detach().clone().to(dtype).requires_grad_(True) for k, v in params.items()}
         self.slices = slices
         self.stash = {}      # (mb, slice) -> (input tensor or None, output tensor)
         self.inbox = {}
@@ -191,7 +191,7 @@ def step_device(dev, a, B, tokens, labels):
         if s < S - 1:
             dev.outbox[(0, mb, s)] = out.detach()
             return (0, mb, s), out.detach()
-        dev.loss += float(out) / B
+        dev.loss += float(out.detach()) / B
         return None
     x_in, out = dev.stash.pop((mb, s))
     if s == S - 1:
@@ -213,11 +213,12 @@ def owner(placement, s):
     return -1
 
 
-def run_local(desc, params, per_device, placement, B, tokens, labels):
-    """Single process, all devices, relaxation order (as src/simulate.cpp)."""
+def run_local(desc, params, per_device, placement, B, tokens, labels, dtype=torch.float64):
+    """Single process, all devices, relaxation order (as src/simulate.cpp).
+    dtype: float64 for parity checks, float32 for the bench's CPU path."""
     us = units(desc)
     bounds = partition(us, slice_devices(placement), len(placement))
-    devs = [Device(desc, params, placement[d], bounds, us) for d in range(len(per_device))]
+    devs = [Device(desc, params, placement[d], bounds, us, dtype) for d in range(len(per_device))]
     published = {}
     pc = [0] * len(devs)
     moved = True
