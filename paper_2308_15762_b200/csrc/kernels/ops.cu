@@ -14,6 +14,7 @@
 
 #include "kernels/gemm.cuh"
 #include "kernels/ops.cuh"
+#include "kernels/softmax_math.cuh"
 
 namespace wpk {
 namespace {
@@ -163,35 +164,49 @@ __global__ void __launch_bounds__(256) ln_fwd_pipe_k(const bf16* x, const float*
       for (int c = 0; c < C; ++c)
         nxt[c] = *reinterpret_cast<const uint4*>(x + static_cast<int64_t>(row + nw) * h + c * 256 + lane * 8);
     }
-    float s = 0.f;
+    // Packed f32x2 arithmetic throughout (FADD2 / FFMA2 / FMUL2): the kernel
+    // is issue-heavy next to its HBM traffic.
+    float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      float v[8];
-      unpack8(cur[c], v);
+      const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&cur[c]);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) s += v[k];
+      for (int k = 0; k < 4; ++k) s2 = smx::fadd2(s2, __bfloat1622float2(hv[k]));
     }
-    const float mu = warp_sum(s) / h;
-    float q = 0.f;
+    const float mu = warp_sum(s2.x + s2.y) / h;
+    const float2 nmu2 = make_float2(-mu, -mu);
+    float2 q2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      float v[8];
-      unpack8(cur[c], v);
+      const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&cur[c]);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) q += (v[k] - mu) * (v[k] - mu);
+      for (int k = 0; k < 4; ++k) {
+        const float2 d = smx::fadd2(__bfloat1622float2(hv[k]), nmu2);
+        q2 = smx::ffma2(d, d, q2);
+      }
     }
-    const float rs = rsqrtf(warp_sum(q) / h + 1e-5f);
+    const float rs = rsqrtf(warp_sum(q2.x + q2.y) / h + 1e-5f);
+    const float2 rs2 = make_float2(rs, rs);
     bf16* yr = y + static_cast<int64_t>(row) * h;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       const int col = c * 256 + lane * 8;
-      float v[8], wv[8], bv[8], o[8];
-      unpack8(cur[c], v);
-      load8(w + col, wv);
-      load8(b + col, bv);
+      const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&cur[c]);
+      const float4 w0 = reinterpret_cast<const float4*>(w + col)[0], w1 = reinterpret_cast<const float4*>(w + col)[1];
+      const float4 b0 = reinterpret_cast<const float4*>(b + col)[0], b1 = reinterpret_cast<const float4*>(b + col)[1];
+      const float2 wv[4] = {make_float2(w0.x, w0.y), make_float2(w0.z, w0.w), make_float2(w1.x, w1.y),
+                            make_float2(w1.z, w1.w)};
+      const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                            make_float2(b1.z, b1.w)};
+      uint4 u;
+      __nv_bfloat162* ho = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) o[k] = (v[k] - mu) * rs * wv[k] + bv[k];
-      store8(yr + col, o);
+      for (int k = 0; k < 4; ++k) {
+        const float2 xh = smx::fmul2(smx::fadd2(__bfloat1622float2(hv[k]), nmu2), rs2);
+        const float2 o = smx::ffma2(xh, wv[k], bv[k]);
+        ho[k] = __floats2bfloat162_rn(o.x, o.y);
+      }
+      *reinterpret_cast<uint4*>(yr + col) = u;
     }
     if (lane == 0) {
       mean[row] = mu;
@@ -453,19 +468,44 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_rows_cs_k(const T* dy, const T*
       const int row = t0 + ty + 32 * k;
       if (row >= T_) break;
       const int64_t off = static_cast<int64_t>(row) * h + col;
-      float d[8], xv[8], r[8], o[8];
-      load8(dy + off, d);
-      load8(x + off, xv);
-      if (dres) load8(dres + off, r);
       const float mu = mean[row], rs = rstd[row], sg = rows[2 * row] * inv_h, sgx = rows[2 * row + 1] * inv_h;
+      if constexpr (std::is_same_v<T, bf16>) {
+        // bf16: packed f32x2 arithmetic (half the FP32 issue slots)
+        const uint4 ud = *reinterpret_cast<const uint4*>(dy + off), ux = *reinterpret_cast<const uint4*>(x + off);
+        const uint4 ur = dres ? *reinterpret_cast<const uint4*>(dres + off) : make_uint4(0u, 0u, 0u, 0u);
+        const __nv_bfloat162* hd = reinterpret_cast<const __nv_bfloat162*>(&ud);
+        const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&ux);
+        const __nv_bfloat162* hr = reinterpret_cast<const __nv_bfloat162*>(&ur);
+        const float2 nmu2 = make_float2(-mu, -mu), rs2 = make_float2(rs, rs);
+        const float2 nsg2 = make_float2(-sg, -sg), nsgx2 = make_float2(-sgx, -sgx);
+        uint4 uo;
+        __nv_bfloat162* ho = reinterpret_cast<__nv_bfloat162*>(&uo);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float xh = (xv[j] - mu) * rs;
-        o[j] = rs * (d[j] * wv[j] - sg - xh * sgx) + (dres ? r[j] : 0.f);
+        for (int k = 0; k < 4; ++k) {
+          const float2 xh = smx::fmul2(smx::fadd2(__bfloat1622float2(hx[k]), nmu2), rs2);
+          float2 t = smx::ffma2(__bfloat1622float2(hd[k]), make_float2(wv[2 * k], wv[2 * k + 1]), nsg2);
+          t = smx::ffma2(xh, nsgx2, t);
+          const float2 o = smx::ffma2(t, rs2, __bfloat1622float2(hr[k]));
+          ho[k] = __floats2bfloat162_rn(o.x, o.y);
+          const float2 orr = __bfloat1622float2(ho[k]);
+          acc[2 * k] += orr.x;
+          acc[2 * k + 1] += orr.y;
+        }
+        *reinterpret_cast<uint4*>(dx + off) = uo;
+      } else {
+        float d[8], xv[8], r[8], o[8];
+        load8(dy + off, d);
+        load8(x + off, xv);
+        if (dres) load8(dres + off, r);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (xv[j] - mu) * rs;
+          o[j] = rs * (d[j] * wv[j] - sg - xh * sgx) + (dres ? r[j] : 0.f);
+        }
+        store8(dx + off, o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += round_to_t<T>(o[j]);
       }
-      store8(dx + off, o);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] += round_to_t<T>(o[j]);
     }
   }
 #pragma unroll
