@@ -366,38 +366,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {
+      // The whole warp walks the loop with warp-uniform state (shared-memory
+      // base from the extern array, TMEM base broadcast, stage / phase from
+      // an induction counter, vote-based barrier waits) and one elected lane
+      // issues: the compiler then keeps the descriptors in uniform registers
+      // and the MMAs go out back to back (see elect_one).
+      const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+      const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
       constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(A_MN) << 15) |
                                  (uint32_t(B_MN) << 16) | (uint32_t(PBN >> 3) << 17) | (uint32_t(PM >> 4) << 24);
-      int stage = 0;
-      uint32_t phase = 0;
+      int it = 0;  // k-blocks consumed (all tiles): stage = it % P_STAGES
       int local = 0;
       for (int u = pair; u < p.num_tiles * p.k_split; u += npairs, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        mbar_wait_warp(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * PBN;
+        const uint32_t tmem_d = tbase + acc * PBN;
         const int kb0 = (u % p.k_split) * p.kb_per, kb1 = min(p.k_blocks, kb0 + p.kb_per);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int stage = it % P_STAGES;
+          mbar_wait_warp(&full_bar[stage], (it / P_STAGES) & 1);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * P_STAGE_BYTES);
+          const uint32_t sa = sbase + stage * P_STAGE_BYTES;
           const uint32_t sb = sa + A_BYTES;
           const uint64_t ad0 = A_MN ? make_desc(sa, CHUNK_BYTES, 1024) : make_desc(sa, 16, 1024);
           const uint64_t bd0 = B_MN ? make_desc(sb, CHUNK_BYTES, 1024) : make_desc(sb, 16, 1024);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            tc_mma_pair(tmem_d, desc_add(ad0, A_MN ? k * 2048 : k * 32), desc_add(bd0, B_MN ? k * 2048 : k * 32), idesc,
-                        (kb != kb0 || k != 0) ? 1u : 0u);
+            if (elect_one())
+              tc_mma_pair(tmem_d, desc_add(ad0, A_MN ? k * 2048 : k * 32), desc_add(bd0, B_MN ? k * 2048 : k * 32),
+                          idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
-          tc_commit_pair(&empty_bar[stage]);  // frees this stage in both CTAs
-          if (++stage == P_STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+          if (elect_one()) tc_commit_pair(&empty_bar[stage]);  // frees this stage in both CTAs
+          __syncwarp();
         }
-        tc_commit_pair(&tfull_bar[acc]);  // both halves of the accumulator ready
+        if (elect_one()) tc_commit_pair(&tfull_bar[acc]);  // both halves of the accumulator ready
+        __syncwarp();
       }
     }
   } else if (warp >= 4 && TE) {

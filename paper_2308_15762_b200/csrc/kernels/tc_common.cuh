@@ -109,6 +109,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// mbar_wait for a whole converged warp with a warp-uniform exit (vote), so
+// the compiler keeps the issuer's loop state in uniform registers.
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  if (__all_sync(0xffffffffu, mbar_try(a, parity))) return;
+  const uint64_t t0 = global_ns();
+  for (uint32_t n = 1;; ++n) {
+    if (__all_sync(0xffffffffu, mbar_try(a, parity))) return;
+    if ((n & 1023u) == 0 && global_ns() - t0 > kMbarTimeoutNs) __trap();
+  }
+}
+
 __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
                                             int c2, int c3) {
   asm volatile(
@@ -396,6 +408,25 @@ __device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uin
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// One lane of a converged warp (elect.sync).  The MMA issuers run their
+// loops in the whole warp with warp-uniform operands (shared-memory base and
+// TMEM base broadcast with __shfl_sync), so the compiler keeps descriptors in
+// uniform registers and issues tcgen05.mma back to back -- about 2 SASS
+// instructions per MMA instead of ~10 (ELECT / R2UR per operand) from a
+// single-lane branch; the issuer shares its SM sub-partition with epilogue /
+// softmax warps, so its issue slots are what keeps the tensor pipe fed.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "elect.sync _|p, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 // Arrive on the barrier at the same offset in both CTAs of the pair.
