@@ -299,8 +299,15 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         }
         t0 += 2 * it.n_max;
       }
-    } else if (warp == 1 && lane == 0) {
+    } else if (warp == 1) {
       // ------------------------------------------------------------- MMA
+      // The whole warp walks the issue loop with warp-uniform state and one
+      // elected lane issues (see elect_one): uniform-register descriptors,
+      // back-to-back MMAs, few issue slots taken from the softmax warps
+      // that share this sub-partition.
+      const uint32_t tb = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t sQa = (smem_u32(smem_raw) + 1023u) & ~1023u;
+      const uint32_t sRa = sQa + 4 * Cfg::TILE;
       // S: M=128, N=128, A=Q K-major, B=K K-major.  PV: M=128, N=D, A=P (TMEM), B=V MN-major.
       constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(KT >> 3) << 17) |
                                    (uint32_t(QT >> 4) << 24);
@@ -311,18 +318,21 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       int npv[2] = {0, 0};     // PV_x issued (all items)
       auto tile_ready = [&](int g) -> uint32_t {  // waits for ring tile g, returns its smem address
         const int slot = g % RING;
-        mbar_wait(&kv_full[slot], (g / RING) & 1);
+        mbar_wait_warp(&kv_full[slot], (g / RING) & 1);
         tc_fence_after();
-        return smem_u32(sR + slot * Cfg::TILE);
+        return sRa + slot * Cfg::TILE;
       };
-      auto free_tile = [&](int g) { tc_commit(&kv_empty[g % RING]); };
+      auto free_tile = [&](int g) {
+        if (elect_one()) tc_commit(&kv_empty[g % RING]);
+        __syncwarp();
+      };
       for (int k = 0;; ++k) {
         const int w = fa_item_index(k);
         if (w >= p.n_items) break;
         const FaItem it = fa_item(p, w);
         const int qb = k & 1;
         const int nkv[2] = {it.nkv0, it.nkv1};
-        mbar_wait(&q_full[qb], (k >> 1) & 1);
+        mbar_wait_warp(&q_full[qb], (k >> 1) & 1);
         tc_fence_after();
         auto issue_s = [&](int x, int j) {
           // PSEP: S_x(j) may overwrite S_x(j-1) once the softmax has it in
@@ -330,34 +340,38 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           // from these columns) in issue order.
           FA_TRACE(8, x, ns[x]);
           if (Cfg::PSEP && ns[x] > 0) {
-            mbar_wait(&s_empty[x], (ns[x] - 1) & 1);
+            mbar_wait_warp(&s_empty[x], (ns[x] - 1) & 1);
             tc_fence_after();
           }
           const uint32_t k_addr = tile_ready(t0 + 2 * j);
-          const uint32_t q_addr = smem_u32(sQ + (2 * qb + x) * Cfg::TILE);
+          const uint32_t q_addr = sQa + (2 * qb + x) * Cfg::TILE;
           FA_TRACE(10, x, ns[x]);
+          const uint64_t qd = make_desc(q_addr, 16, 1024), kd = make_desc(k_addr, 16, 1024);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
-            tc_mma(tmem + Cfg::col_s(x), make_desc(q_addr + off, 16, 1024), make_desc(k_addr + off, 16, 1024),
-                   idesc_s, kk != 0);
+            if (elect_one()) tc_mma(tb + Cfg::col_s(x), desc_add(qd, off), desc_add(kd, off), idesc_s, kk != 0);
           }
-          tc_commit(&s_full[x]);
+          if (elect_one()) tc_commit(&s_full[x]);
+          __syncwarp();
           FA_TRACE(1, x, ns[x]);
           ++ns[x];
         };
         auto issue_pv = [&](int x, int j) {
           FA_TRACE(9, x, npv[x]);
-          mbar_wait(&p_full[x], npv[x] & 1);
+          mbar_wait_warp(&p_full[x], npv[x] & 1);
           tc_fence_after();
           const uint32_t v_addr = tile_ready(t0 + 2 * j + 1);
           FA_TRACE(11, x, npv[x]);
+          const uint64_t vd = make_desc(v_addr, ATOM, 1024);
 #pragma unroll
           for (int kk = 0; kk < KT / 16; ++kk) {
-            const uint64_t bd = make_desc(v_addr + kk * 2048, ATOM, 1024);
-            tc_mma_ts(tmem + Cfg::col_o(x), tmem + Cfg::col_p(x) + kk * 8, bd, idesc_pv, (j | kk) != 0);
+            if (elect_one())
+              tc_mma_ts(tb + Cfg::col_o(x), tb + Cfg::col_p(x) + kk * 8, desc_add(vd, kk * 2048), idesc_pv,
+                        (j | kk) != 0);
           }
-          tc_commit(&o_done[x]);
+          if (elect_one()) tc_commit(&o_done[x]);
+          __syncwarp();
           FA_TRACE(2, x, npv[x]);
           ++npv[x];
         };
@@ -398,7 +412,10 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
               }
             }
           }
-          if (j + 2 == it.n_max || it.n_max == 1) tc_commit(&q_empty[qb]);  // every S of the item issued
+          if (j + 2 == it.n_max || it.n_max == 1) {  // every S of the item issued
+            if (elect_one()) tc_commit(&q_empty[qb]);
+            __syncwarp();
+          }
         }
         t0 += 2 * it.n_max;
       }
