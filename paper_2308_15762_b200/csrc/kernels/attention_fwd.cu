@@ -156,10 +156,10 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint
 }
 
 // POLY: of every 8 column pairs of an S row, this many take the polynomial
-// 2^x.  D = 128 tiles balance the SFU against the tensor core, D = 64 tiles
-// (half the MMA work per exponential) lean on the FMA pipe harder.
+// 2^x (3 = 37.5 % at both D: measured best with 2, ahead of 0 and of 4-5,
+// which cost more FMA-pipe issue than they save on the SFU).
 // WP_FA_POLY=n (0, 2-5) overrides for A/B.
-constexpr int kFaPolyD128 = 3, kFaPolyD64 = 4;
+constexpr int kFaPolyD128 = 3, kFaPolyD64 = 3;
 
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
   asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
