@@ -59,8 +59,10 @@ namespace {
 using namespace tc;
 using namespace smx;
 
-// Of every 8 column pairs of a P^T row, this many take the FMA-pipe 2^x.
-constexpr int kBwPoly = 2;
+// Of every 8 column pairs of a P^T row, this many take the FMA-pipe 2^x
+// (0: measured 0 / 2 / 4 -> the backward is not SFU-bound; 0 is 1-3 %
+// ahead of 2 at D 64 and even at D 128).
+constexpr int kBwPoly = 0;
 
 constexpr int T128 = 128;
 constexpr int ATOM = 128 * 64 * 2;  // SW128 atom: 128 rows x 64 bf16
