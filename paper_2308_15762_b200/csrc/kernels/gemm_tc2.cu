@@ -51,7 +51,7 @@ struct PairCfg {
 template <int CPC>
 __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map_c, const CUtensorMap* map_x,
                                          uint8_t* slabs, uint64_t* sbar, uint32_t& sphase, int& buf, uint32_t taddr,
-                                         int gcol, int row0, int lane, const float* bias) {
+                                         int gcol, int row0, int lane, const float* bias, bool prefetched = false) {
   const Epilogue& e = p.epi;
   const int mode = e.mode;
   constexpr int dt = CPC == 32 ? kF32 : kBF16;
@@ -62,13 +62,15 @@ __device__ __forceinline__ void epi_slab(const Params& p, const CUtensorMap* map
   const bool aux2 = ln || rd;                      // a second input slab, loaded into xb
   const int xb = buf ^ 1;                          // the LN input slab (buf flips below)
   uint8_t* sx = slabs + xb * SLAB_BYTES;
-  if (lane == 0) {
+  // prefetched: the input slab was loaded (into slab `buf`) by the caller a
+  // tile ahead, after the slabs' previous stores had read them
+  if (lane == 0 && !prefetched) {
     // the slab(s) about to be written must have been read out by earlier stores
     if (mode == kEpiGelu || aux2) bulk_wait_read<0>();
     else bulk_wait_read<1>();
   }
   __syncwarp();
-  if (needs_in && lane == 0) {
+  if (needs_in && lane == 0 && !prefetched) {
     mbar_expect_tx(&sbar[buf], SLAB_BYTES);
     tma_load_2d(map_x, &sbar[buf], sb, gcol, row0);
   }
@@ -416,6 +418,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint32_t sphase = 0;
     int buf = 0;
     int local = 0;
+    // dGELU with a bf16 C: the warp's two 64-column pre-activation slabs of a
+    // tile are loaded one tile ahead (once the previous tile's stores have
+    // read the slabs), so their latency hides behind the mainloop -- what
+    // the short-K FC2 data gradients (K = hidden) need; the residual mode
+    // measured better without it.
+    const bool pre = p.epi.mode == kEpiDGelu && !f32 && !p.epi.ln_x && !p.epi.rd_x;
+    auto prefetch = [&](int u) {
+      int mb, nb;
+      decode_tile_grouped(p, u / p.k_split, mb, nb);
+      const int row0 = mb * PM + static_cast<int>(rank) * BM + ew * 32;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int gcol = nb * PBN + half * (PBN / 2) + i * 64;
+        if (gcol >= p.N) break;
+        mbar_expect_tx(&sbar[i], SLAB_BYTES);
+        tma_load_2d(&map_x, &sbar[i], slabs + i * SLAB_BYTES, gcol, row0);
+      }
+    };
+    if (pre && lane == 0 && pair < p.num_tiles * p.k_split) prefetch(pair);
     for (int u = pair; u < p.num_tiles * p.k_split; u += npairs, ++local) {
       int mb, nb;
       decode_tile_grouped(p, u / p.k_split, mb, nb);
@@ -426,15 +447,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int row0 = mb * PM + static_cast<int>(rank) * BM + ew * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * PBN;
-      for (int c = half * (PBN / 2); c < (half + 1) * (PBN / 2); c += cpc) {
+      for (int c = half * (PBN / 2), i = 0; c < (half + 1) * (PBN / 2); c += cpc, ++i) {
         const int gcol = nb * PBN + c;
         if (gcol >= p.N) break;
+        if (pre) buf = i;
         if (f32) epi_slab<32>(p, &map_c, &map_x, slabs, sbar, sphase, buf, taddr + c, gcol, row0, lane, bias);
-        else epi_slab<64>(p, &map_c, &map_x, slabs, sbar, sphase, buf, taddr + c, gcol, row0, lane, bias);
+        else epi_slab<64>(p, &map_c, &map_x, slabs, sbar, sphase, buf, taddr + c, gcol, row0, lane, bias, pre);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 0);
+      if (pre && lane == 0 && u + npairs < p.num_tiles * p.k_split) {
+        bulk_wait_read<0>();  // this tile's stores have read both slabs
+        prefetch(u + npairs);
+      }
     }
     if (lane == 0) bulk_wait<0>();
   } else if (warp >= 4) {
