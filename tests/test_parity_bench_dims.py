@@ -94,3 +94,24 @@ def test_fp32_parity_gpt13b_widths_seq256():
     errs = {name: rel(got[name], ref[name]) for name in ref}
     bad = {k: v for k, v in errs.items() if v > 1e-5}
     assert not bad, bad
+
+
+@pytest.mark.parametrize("name,widths,seq,causal", [
+    ("gpt2-medium", dict(layers=2, hidden=1024, heads=16, ffn=4096, vocab=50304, micro_batch_size=1), 1024, True),
+    ("bert-large", dict(layers=2, hidden=1024, heads=16, ffn=4096, vocab=30528, micro_batch_size=1), 512, False),
+])
+def test_bf16_parity_c2_c3_widths(name, widths, seq, causal):
+    """BASELINE configs 2 and 3 at their own widths (d=64 heads; BERT-large
+    bidirectional with labels on every position), Hanayo P=2 W=2 on one GPU,
+    against the bf16 rounding-point oracle: same stated tolerance."""
+    desc = wp.ModelDesc(**widths, seq=seq, dtype="bf16", causal=causal)
+    odesc = wp.ModelDesc(**widths, seq=seq, causal=causal)
+    params = om.init_params(odesc, seed=6)
+    tokens, labels = synthetic_batch(B, 1, seq, widths["vocab"], causal=causal)
+    ref_loss, ref = om.reference_step(params, tokens, labels, odesc, emulate="bf16")
+    ref = {k: v.numpy().ravel() for k, v in ref.items()}
+    loss, got = gpu_step(desc, 2, params, tokens, labels)
+    assert np.isfinite(loss) and abs(loss - ref_loss) <= 2e-3 * abs(ref_loss), (name, loss, ref_loss)
+    errs = {k: rel(got[k], ref[k]) for k in ref}
+    bad = {k: v for k, v in errs.items() if v > 1e-2}
+    assert not bad, (name, bad)
