@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       const uint32_t tb = __shfl_sync(0xffffffffu, tmem, 0);
       const uint32_t sQa = (smem_u32(smem_raw) + 1023u) & ~1023u;
       const uint32_t sRa = sQa + 4 * Cfg::TILE;
+      if (sQa != smem_u32(sQ)) __trap();  // shared-space and generic alignment must agree
       // S: M=128, N=128, A=Q K-major, B=K K-major.  PV: M=128, N=D, A=P (TMEM), B=V MN-major.
       constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(KT >> 3) << 17) |
                                    (uint32_t(QT >> 4) << 24);

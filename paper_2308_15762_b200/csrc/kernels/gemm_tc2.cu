@@ -376,6 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       // and the MMAs go out back to back (see elect_one).
       const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
       const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+      if (sbase != smem_u32(smem)) __trap();  // shared-space and generic alignment must agree
       constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(A_MN) << 15) |
                                  (uint32_t(B_MN) << 16) | (uint32_t(PBN >> 3) << 17) | (uint32_t(PM >> 4) << 24);
       int it = 0;  // k-blocks consumed (all tiles): stage = it % P_STAGES
