@@ -115,3 +115,30 @@ def test_bf16_parity_c2_c3_widths(name, widths, seq, causal):
     errs = {k: rel(got[k], ref[k]) for k in ref}
     bad = {k: v for k, v in errs.items() if v > 1e-2}
     assert not bad, (name, bad)
+
+
+def test_bf16_parity_waves4_empty_slices():
+    """Hanayo P=2 W=4 (S = 16 slices over a 4-layer model's 10 units, so
+    some slices are empty and messages cross them unchanged) at the
+    GPT2-medium widths, bf16, against the bf16 rounding-point oracle."""
+    widths = dict(layers=4, hidden=1024, heads=16, ffn=4096, vocab=50304, micro_batch_size=1)
+    seq = 512
+    desc = wp.ModelDesc(**widths, seq=seq, dtype="bf16")
+    odesc = wp.ModelDesc(**widths, seq=seq)
+    params = om.init_params(odesc, seed=8)
+    Bw = 4
+    tokens, labels = synthetic_batch(Bw, 1, seq, widths["vocab"])
+    ref_loss, ref = om.reference_step(params, tokens, labels, odesc, emulate="bf16")
+    ref = {k: v.numpy().ravel() for k, v in ref.items()}
+    sched = wp.generate_schedule(wp.make_config(wp.Scheme.Hanayo, 2, Bw, 4))
+    rt = wp.Runtime(desc, sched, device_ids=[0, 0])
+    for name, t in params.items():
+        rt.set_param(name, t.numpy())
+    rt.set_update(False)
+    loss = rt.train_step(tokens, labels)
+    got = {name: rt.get_grad(name, n) for name, n in rt.param_names()}
+    rt.close()
+    assert np.isfinite(loss) and abs(loss - ref_loss) <= 2e-3 * abs(ref_loss), (loss, ref_loss)
+    errs = {k: rel(got[k], ref[k]) for k in ref}
+    bad = {k: v for k, v in errs.items() if v > 1e-2}
+    assert not bad, bad
