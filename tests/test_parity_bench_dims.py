@@ -142,3 +142,34 @@ def test_bf16_parity_waves4_empty_slices():
     errs = {k: rel(got[k], ref[k]) for k in ref}
     bad = {k: v for k, v in errs.items() if v > 1e-2}
     assert not bad, bad
+
+
+@pytest.mark.parametrize("scheme", [wp.Scheme.Dapple, wp.Scheme.ChimeraWave])
+def test_bf16_parity_baseline_schemes_widths(scheme):
+    """The baseline schemes through the same runtime at the GPT2-medium
+    widths, bf16: DAPPLE P=2 (classic placement: untied LM head) and
+    Chimera-wave P=2 W=2 (Hanayo placement, tied), against the bf16
+    rounding-point oracle."""
+    tied = scheme == wp.Scheme.ChimeraWave
+    widths = dict(layers=2, hidden=1024, heads=16, ffn=4096, vocab=50304, micro_batch_size=1)
+    seq = 512
+    desc = wp.ModelDesc(**widths, seq=seq, dtype="bf16", tie_embeddings=tied)
+    odesc = wp.ModelDesc(**widths, seq=seq, tie_embeddings=tied)
+    params = om.init_params(odesc, seed=9)
+    Bs = 4
+    tokens, labels = synthetic_batch(Bs, 1, seq, widths["vocab"])
+    ref_loss, ref = om.reference_step(params, tokens, labels, odesc, emulate="bf16")
+    ref = {k: v.numpy().ravel() for k, v in ref.items()}
+    W = 2 if tied else 1
+    sched = wp.generate_schedule(wp.make_config(scheme, 2, Bs, W))
+    rt = wp.Runtime(desc, sched, device_ids=[0, 0])
+    for name, t in params.items():
+        rt.set_param(name, t.numpy())
+    rt.set_update(False)
+    loss = rt.train_step(tokens, labels)
+    got = {name: rt.get_grad(name, n) for name, n in rt.param_names()}
+    rt.close()
+    assert np.isfinite(loss) and abs(loss - ref_loss) <= 2e-3 * abs(ref_loss), (loss, ref_loss)
+    errs = {k: rel(got[k], ref[k]) for k in ref}
+    bad = {k: v for k, v in errs.items() if v > 1e-2}
+    assert not bad, bad
