@@ -38,8 +38,10 @@ def _free_port():
 
 
 def _desc(dtype, optimizer="sgd", tie=True):
+    import json
     import paper_2308_15762_b200 as wp
-    return wp.ModelDesc(**TINY, dtype=dtype, optimizer=optimizer, lr=1e-3, weight_decay=0.01, tie_embeddings=tie)
+    widths = json.loads(os.environ["WP_TEST_WIDTHS"]) if os.environ.get("WP_TEST_WIDTHS") else TINY
+    return wp.ModelDesc(**widths, dtype=dtype, optimizer=optimizer, lr=1e-3, weight_decay=0.01, tie_embeddings=tie)
 
 
 def _run(rt, params, B, desc, steps, update, replica=0):
@@ -391,3 +393,28 @@ def test_measured_compare_tool_two_ranks():
     spans = [float(r[4]) for r in rows if r[4]]
     assert spans == sorted(spans) and all(0 < s < 60 for s in spans)
     assert all(0.0 <= float(r[5]) < 1.0 for r in rows if r[5])
+
+
+def test_ipc_bf16_gpt2_medium_widths_equal_oracle():
+    """Two processes over CUDA IPC at the GPT2-medium widths (BASELINE
+    config 2's layer shapes, d=64 heads), Hanayo P=2 W=2, bf16: loss and
+    every gradient against the bf16 rounding-point oracle (1e-2 normwise,
+    the stated bf16 tolerance), messages of mbs x seq x hidden bf16."""
+    import json
+    from oracle import model as om
+    from paper_2308_15762_b200.data import synthetic_batch
+    widths = dict(layers=2, hidden=1024, heads=16, ffn=4096, seq=512, vocab=50304, micro_batch_size=1)
+    os.environ["WP_TEST_WIDTHS"] = json.dumps(widths)
+    try:
+        losses, grads = _spawn(2, 4, 2, "bf16")
+        desc = _desc("fp32")
+    finally:
+        del os.environ["WP_TEST_WIDTHS"]
+    params = om.init_params(desc, seed=21)
+    tokens, labels = synthetic_batch(4, 1, widths["seq"], widths["vocab"])
+    want_loss, want = om.reference_step(params, tokens, labels, desc, emulate="bf16")
+    assert abs(losses[0] - want_loss) <= 2e-3 * abs(want_loss), (losses[0], want_loss)
+    for n, g in want.items():
+        w = g.numpy().ravel().astype(np.float64)
+        e = np.linalg.norm(grads[n].astype(np.float64) - w) / max(np.linalg.norm(w), 1e-30)
+        assert e <= 1e-2, (n, e)
